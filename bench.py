@@ -1,0 +1,328 @@
+"""bench.py -- 4K UHD frames/s (min face 60 px) and stage-1 Gwindows/s of the B200 hot path.
+
+Contract:
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config c4]
+  N > 1: launched by torchrun, one rank per GPU, frames sharded by rank (weak scaling);
+  NCCL is used once, for the final all_gather of the detections.
+A step = one ccnn_detect over one batch of synthetic frames (pyramid -> fused stage 1 ->
+selective unit -> NMS -> boxes on the host).  `value` is timed with CUDA events on the
+ctx stream with the batch already resident in HBM (265 MB of 4K frames per step, larger
+than the 126 MB L2); `e2e` is the same call with the frames in pinned HOST memory
+(H2D inside the timed region).  Rank 0 prints ONE JSON line.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_4K_FPS = 27.0   # PAPER.md P:17 / P:245-255 (mobile Kepler + Ivy Bridge): context
+
+
+def stage1_alg_flops(levels):
+    """Algorithmic stage-1 FLOPs of one frame: 2 x MACs of the dense fully-convolutional
+    CNN1 over the conv outputs some window needs."""
+    tot = 0
+    for _, lw, lh in levels:
+        nx, ny = (lw - 27) // 4 + 1, (lh - 31) // 4 + 1
+        macs = ((4 * nx + 20) * (4 * ny + 24) * 6 * 16      # C4x4 1->6
+                + (2 * nx + 8) * (2 * ny + 10) * 6 * 54      # C3x3 6->6
+                + nx * ny * (2 * 180 + 2))                   # C5x6 6->2, C1x1 2->1
+        tot += 2 * macs
+    return tot
+
+
+def level_table(W, H, min_face, sf):
+    """Level sizes for reporting (same O1 rule as the library; floats only for counting)."""
+    out = []
+    s = 27.0 / min_face
+    sfd = float(np.float32(sf))
+    while True:
+        lw, lh = int(np.floor(W * s)), int(np.floor(H * s))
+        if lw < 27 or lh < 31:
+            break
+        out.append((s, lw, lh))
+        s = s / sfd
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 4 + k and r[4 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def cpu_baseline(cfg, cascade_ws, frames, T1, T2, budget_s=20.0):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the workload."""
+    import oracle
+    from synth import arch
+    cas = oracle.Cascade(arch.NETS, cascade_ws)
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    n = 0
+    while n < len(frames):
+        oracle.detect(cas, frames[n:n + 1], cfg.min_face, cfg.scale_step, T1, T2, cfg.Tnn,
+                      cfg.rule, n_threads=cores)
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "frames/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} of the bench's {cfg.width}x{cfg.height} frames through oracle.detect "
+                      f"(C, fp64, dense stage-1 scan, {cores} threads), {dt:.1f} s"}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the oracle (the only reference this tier has), on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from synth import weights
+    ws = weights.make_cascade_weights()
+    T1, T2 = cfg.thresholds()
+    frames = cfg.make_frames(max(1, args.warmup + args.steps))
+    import oracle
+    from synth import arch
+    cas = oracle.Cascade(arch.NETS, ws)
+    cores = len(os.sched_getaffinity(0))
+    for k in range(args.warmup):
+        oracle.detect(cas, frames[k:k + 1], cfg.min_face, cfg.scale_step, T1, T2, cfg.Tnn, cfg.rule)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        f = args.warmup + k
+        oracle.detect(cas, frames[f:f + 1], cfg.min_face, cfg.scale_step, T1, T2, cfg.Tnn, cfg.rule)
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    line = {"impl": "reference", "metric": "4K UHD frames/s (min face 60px)", "value": v,
+            "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": v / PAPER_4K_FPS, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "frames_per_step": 1, "W": cfg.width, "H": cfg.height,
+                       "min_face": cfg.min_face, "scale_step": cfg.scale_step},
+            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": cores, "kind": "oracle",
+                             "sample": f"1 frame per step of {cfg.name} through oracle.detect"},
+            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--batch", type=int, default=0, help="frames per step per GPU (0 = config)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from synth import configs, weights
+    cfg = configs.BY_ID[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    from paper_1508_01292_b200 import Detector
+    from synth import arch
+    ws = weights.make_cascade_weights()
+    T1, T2 = cfg.thresholds()
+    batch = args.batch or cfg.batch
+    # frame-sharded weak scaling: rank r owns its own stream segment (frames are independent)
+    frames = cfg.make_frames(batch, seed=configs.FRAME_SEED + 7919 * rank)
+    det = Detector(arch.NETS, ws, T1, T2, cfg.Tnn, cfg.rule, max_w=cfg.width, max_h=cfg.height,
+                   max_batch=batch, queue_capacity=max(4096, 40000 if cfg.kind == "clutter" else 0),
+                   device=dev.index)
+    stream = torch.cuda.current_stream(dev)
+    det.set_stream(stream.cuda_stream)
+    dframes = torch.from_numpy(frames).to(dev)
+    levels = level_table(cfg.width, cfg.height, cfg.min_face, cfg.scale_step)
+    windows_per_frame = sum(((w - 27) // 4 + 1) * ((h - 31) // 4 + 1) for _, w, h in levels)
+    flops_per_frame = stage1_alg_flops(levels)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        det.detect(dframes, cfg.min_face, cfg.scale_step)
+    clocks = ClockSampler(dev.index) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s1_ms, launches, all_boxes = 0.0, 0, []
+    stats = None
+    e0.record(stream)
+    for _ in range(args.steps):
+        b = det.detect(dframes, cfg.min_face, cfg.scale_step)
+        stats = det.last_stats
+        s1_ms += stats["ms"][2]
+        launches += stats["kernel_launches"]
+        all_boxes.append(b)
+    # the only cross-GPU exchange: gather every rank's detections (NCCL), once
+    if dist is not None:
+        mine = torch.from_numpy(np.ascontiguousarray(all_boxes[-1]).view(np.int32).reshape(-1, 7)).to(dev)
+        cnt = torch.tensor([mine.shape[0]], device=dev, dtype=torch.int64)
+        cnts = [torch.zeros_like(cnt) for _ in range(world)]
+        dist.all_gather(cnts, cnt)
+        mx = int(max(int(c.item()) for c in cnts))
+        pad = torch.zeros((max(mx, 1), 7), dtype=torch.int32, device=dev)
+        pad[:mine.shape[0]] = mine
+        gath = [torch.zeros_like(pad) for _ in range(world)]
+        dist.all_gather(gath, pad)
+    e1.record(stream)
+    e1.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clk = clocks.stop() if clocks else None
+
+    # ---- e2e: same call with the frames in pinned host memory (H2D inside the timed region)
+    e2e_steps = args.e2e_steps or max(3, args.steps // 2)
+    host = torch.from_numpy(frames).pin_memory()
+    det.detect(host, cfg.min_face, cfg.scale_step)
+    barrier()
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record(stream)
+    d2h = 0
+    for _ in range(e2e_steps):
+        b = det.detect(host, cfg.min_face, cfg.scale_step)
+        d2h += b.nbytes + 64
+    h1.record(stream)
+    h1.synchronize()
+    barrier()
+    ms_e2e = h0.elapsed_time(h1)
+    if dist is not None:
+        t = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+
+    if rank == 0:
+        total_frames = world * batch * args.steps
+        value = total_frames / (ms / 1000.0)
+        s1_avg_ms = s1_ms / args.steps
+        achieved_tflops = flops_per_frame * batch / (s1_avg_ms / 1000.0) / 1e12
+        peaks = measured_peaks()
+        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+        fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12     # FFMA pipe peak
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "stage1_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get("bytes_per_launch_per_frame")
+                traffic = traffic * batch if traffic else None
+            except Exception:
+                traffic = None
+        line = {
+            "metric": "4K UHD frames/s (min face 60px)",
+            "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": value / PAPER_4K_FPS, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "frames_per_step_per_gpu": batch, "W": cfg.width,
+                       "H": cfg.height, "min_face": cfg.min_face, "scale_step": cfg.scale_step,
+                       "Tnn": cfg.Tnn, "levels": len(levels), "windows_per_frame": windows_per_frame,
+                       "parallelism": f"frame-sharded dp{world}",
+                       "l2": "inputs larger than L2 (%.0f MB frames/step/GPU)" % (frames.nbytes / 1e6)},
+            "stage1_gwindows_per_s": windows_per_frame * batch / (s1_avg_ms / 1000.0) / 1e9 * world,
+            "pipeline_gwindows_per_s": windows_per_frame * total_frames / (ms / 1000.0) / 1e9,
+            "stage_ms_per_step": {k: v for k, v in zip(["h2d", "pyramid", "stage1", "selective", "nms_out"],
+                                                        stats["ms"])},
+            "table1_counts_last_step": {k: stats[k] for k in ("windows", "stage1", "stage2", "stage3", "nms")},
+            "roofline": {"bound": "alu", "achieved": achieved_tflops, "peak": fp32_peak,
+                         "unit": "TFLOP/s", "frac": achieved_tflops / fp32_peak, "traffic": traffic,
+                         "kernel": "stage1_kernel",
+                         "peak_note": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)"},
+            "e2e": {"value": world * batch * e2e_steps / (ms_e2e / 1000.0), "unit": "frames/s",
+                    "h2d_bytes_per_step": int(frames.nbytes), "d2h_bytes_per_step": int(d2h // e2e_steps)},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(cfg, ws, frames, T1, T2)
+        elif not args.no_cpu_baseline:
+            line["cpu_baseline"] = None
+        print(json.dumps(line), flush=True)
+    det.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

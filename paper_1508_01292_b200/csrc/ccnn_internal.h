@@ -1,0 +1,107 @@
+// ccnn_internal.h -- device data layout and launcher declarations shared by the
+// runtime (runtime.cu) and the sm_100a kernels.  Not part of the ABI.
+//
+// Architecture R (R1; §3.1, Fig. 1 missing) is compiled in:
+//   CNN1: C4x4 1->6, P, C3x3 6->6, P, C5x6 6->2, C1x1 2->1     (27x31 window, stride 4)
+//   CNN2: C4x4 1->16, P, C3x3 16->6, P, C7x8 6->2, C1x1 2->1   (51x55 -> 5x5)
+//   CNN3: C4x4 1->2, P, C3x3 2->2, P, C7x8 2->25, C1x1 25->1   (51x55 -> 5x5)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ccnn {
+
+constexpr int kWinW = 27, kWinH = 31;           // stage-1 window
+constexpr int kStep = 4;                        // window step
+constexpr int kPatchW = 51, kPatchH = 55;       // selective patch
+constexpr int kPatchN = kPatchW * kPatchH;      // 2805
+constexpr int kResp = 25;                       // 5x5 response map
+
+// ---- weights, laid out for compile-time indexing (kernel parameters = constant bank) ----
+struct Cnn1W {                 // 797 floats
+    float w1[6][16], b1[6];    // [out][ky*4+kx]
+    float w2[6][6][9], b2[6];  // [out][in][ky*3+kx]
+    float w3[2][6][30], b3[2]; // [out][in][ky*5+kx]
+    float w4[2], b4;
+};
+template <int A, int B, int C>
+struct SelNetW {               // CNN2: <16,6,2>, CNN3: <2,2,25>
+    float w1[A][16], b1[A];
+    float w2[B][A][9], b2[B];
+    float w3[C][B][56], b3[C]; // [out][in][ky*7+kx], 7 wide x 8 tall
+    float w4[C], b4;
+};
+using Cnn2W = SelNetW<16, 6, 2>;
+using Cnn3W = SelNetW<2, 2, 25>;
+
+// ---- per-call geometry ----
+struct LevelInfo {             // one pyramid level (same for every frame of a batch)
+    double sigma;
+    int64_t offset;            // byte offset of the level inside one frame's level arena
+    int32_t lw, lh, pitch;     // level size, row pitch (multiple of 16 B)
+    int32_t nx, ny;            // window grid
+    int32_t map_off;           // offset of the level in one frame's dense stage-1 map (debug)
+    int32_t tab_off;           // offset of the level's x table (lw entries) then y table (lh)
+    int32_t row0;              // first row of the level in the concatenation of all levels
+};
+struct S1Task {                // one stage-1 CTA task: a band of windows on one level
+    int32_t frame;
+    int16_t level, bw;         // level, band width in windows (<= TW)
+    int16_t x0, y0;            // first window column / row
+    int16_t nrows, pad;        // window rows in this task
+};
+struct S1Cand {                // stage-1 survivor record (16 B)
+    int32_t frame;
+    int16_t level, pad;
+    int16_t ix, iy;            // window column j / row i
+    float s1;
+};
+struct SelOut {                // selective-unit outcome per survivor
+    int32_t K2, K3, delta, cnn3_ran;
+    float score;
+    int32_t bx, by, bw, bh;
+};
+struct AccBox {                // accepted raw box (O8)
+    int32_t frame, x, y, w, h;
+    float score;
+};
+struct OutBox { int32_t frame, x, y, w, h; float score; int32_t neighbors; };
+
+// device control block, zeroed at the start of every detect
+struct Ctrl {
+    uint32_t task_next;        // stage-1 dynamic task counter
+    uint32_t n_cand;           // stage-1 survivors (may exceed capacity -> error)
+    uint32_t sel_next;         // selective dynamic work counter
+    uint32_t n_stage2, n_stage3;
+    uint32_t n_acc;            // accepted raw boxes
+    uint32_t nms_done;         // NMS last-block ticket
+    uint32_t n_out;            // boxes after NMS
+    uint32_t nms_overflow;     // a frame exceeded the NMS capacity
+    uint32_t pad[7];
+};
+
+constexpr int kNmsCap = 4096;  // raw boxes per frame handled by one NMS CTA
+
+// ---- launchers (stream-ordered, no sync) ----
+// pyramid: every level of every frame from the original frames
+void launch_pyramid(const uint8_t* frames, int64_t frame_stride, int64_t pitch, int W, int H,
+                    uint8_t* levels, int64_t level_frame_stride, const LevelInfo* d_levels,
+                    const LevelInfo* h_levels, int n_levels, const uint32_t* d_tabs, int n,
+                    cudaStream_t s);
+// stage 1 (fused CNN1 + threshold + compaction), persistent over the task table
+void launch_stage1(const Cnn1W& w, float T1, const uint8_t* levels, int64_t level_frame_stride,
+                   const LevelInfo* d_levels, const S1Task* d_tasks, int n_tasks, S1Cand* cands,
+                   uint32_t cand_cap, Ctrl* ctrl, float* dbg_map, int64_t dbg_map_frame_stride,
+                   int sm_count, cudaStream_t s);
+int stage1_band_width();       // TW of the compiled stage-1 kernel
+// selective unit (stage 2/3), persistent over the survivor queue
+struct SelParams { float T2a, T2b; int32_t Tnn, rule; };
+void launch_selective(const Cnn2W& w2, const Cnn3W& w3, SelParams sp, const uint8_t* frames,
+                      int64_t frame_stride, int64_t pitch, int W, int H, const LevelInfo* d_levels,
+                      const S1Cand* cands, uint32_t cand_cap, SelOut* out, float* dbg_resp,
+                      AccBox* acc, Ctrl* ctrl, int sm_count, cudaStream_t s);
+// grouping / NMS per frame + compaction of the results
+void launch_nms(const AccBox* acc, Ctrl* ctrl, int n_frames, int min_cluster, OutBox* staging,
+                int32_t* frame_counts, OutBox* out, cudaStream_t s);
+
+}  // namespace ccnn

@@ -1,0 +1,182 @@
+// nms.cu -- grouping / NMS of accepted regions on device (K4).
+//
+// PAPER.md §3.3: "The last stage of the pipeline detector is Non-Maximum
+// Suppression (NMS) algorithm, which aggregates the found regions to form the resulting
+// areas of faces localization."  No parameters are given; reading O9 (SPEC S:332,
+// S:357): transitive grouping of the raw boxes whose IoU >= 0.3 (exact integer test
+// 10*inter >= 3*union), components smaller than nms_min_cluster dropped, per component
+// the coordinate mean rounded half up ((2*sum + n) div 2n), the max score, neighbours =
+// size; output sorted by (frame, score desc, y, x, w, h).  Integer sums make the result
+// independent of the (nondeterministic) order in which accepted boxes arrive.
+//
+// One CTA per frame, everything in shared memory: lock-free union-find (hook the larger
+// root under the smaller), shared-memory atomics for the per-component sums, rank sort.
+// The last CTA to finish (ticket) compacts all frames' results into one array.
+#include "ccnn_internal.h"
+
+namespace ccnn {
+namespace {
+
+constexpr int kNmsThreads = 512;
+
+struct NmsSmem {
+    short4 box[kNmsCap];         // x, y, w, h of this frame's raw boxes
+    float score[kNmsCap];
+    int parent[kNmsCap];
+    int sx[kNmsCap], sy[kNmsCap], sw[kNmsCap], sh[kNmsCap], cnt[kNmsCap];
+    int best[kNmsCap];           // order-preserving int image of the max score
+    int n, m, is_last;
+};
+
+__device__ __forceinline__ int f2ord(float f)
+{
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+
+__device__ __forceinline__ bool iou_edge(short4 a, short4 b)
+{
+    const long long ix = (long long)min(a.x + a.z, b.x + b.z) - max(a.x, b.x);
+    const long long iy = (long long)min(a.y + a.w, b.y + b.w) - max(a.y, b.y);
+    if (ix <= 0 || iy <= 0) return false;
+    const long long inter = ix * iy;
+    const long long uni = (long long)a.z * a.w + (long long)b.z * b.w - inter;
+    return 10 * inter >= 3 * uni;
+}
+
+__device__ __forceinline__ int find_root(volatile int* parent, int k)
+{
+    while (true) {
+        const int p = parent[k];
+        if (p == k) return k;
+        k = p;
+    }
+}
+
+__device__ __forceinline__ void unite(int* parent, int a, int b)
+{
+    for (;;) {
+        a = find_root(parent, a);
+        b = find_root(parent, b);
+        if (a == b) return;
+        if (a < b) { const int t = a; a = b; b = t; }       // hook larger root under smaller
+        if (atomicCAS(&parent[a], a, b) == a) return;
+    }
+}
+
+// total order: score desc, y, x, w, h, then slot (ties only between identical boxes)
+__device__ __forceinline__ bool before(const OutBox& a, int ia, const OutBox& b, int ib)
+{
+    if (a.score != b.score) return a.score > b.score;
+    if (a.y != b.y) return a.y < b.y;
+    if (a.x != b.x) return a.x < b.x;
+    if (a.w != b.w) return a.w < b.w;
+    if (a.h != b.h) return a.h < b.h;
+    return ia < ib;
+}
+
+__global__ void __launch_bounds__(kNmsThreads) nms_kernel(
+    const AccBox* __restrict__ acc, Ctrl* __restrict__ ctrl, const int n_frames,
+    const int min_cluster, OutBox* __restrict__ staging, int32_t* __restrict__ frame_counts,
+    OutBox* __restrict__ out)
+{
+    extern __shared__ __align__(16) unsigned char sraw[];
+    NmsSmem& sm = *reinterpret_cast<NmsSmem*>(sraw);
+    const int tid = threadIdx.x;
+    const int f = blockIdx.x;
+    const int n_acc = (int)*(volatile uint32_t*)&ctrl->n_acc;
+    if (tid == 0) { sm.n = 0; sm.m = 0; }
+    __syncthreads();
+    for (int k = tid; k < n_acc; k += kNmsThreads) {
+        const AccBox b = acc[k];
+        if (b.frame != f) continue;
+        const int s = atomicAdd(&sm.n, 1);
+        if (s < kNmsCap) {
+            sm.box[s] = make_short4((short)b.x, (short)b.y, (short)b.w, (short)b.h);
+            sm.score[s] = b.score;
+        }
+    }
+    __syncthreads();
+    const int n = sm.n;
+    // staging per frame: [0, kNmsCap) unsorted groups, [kNmsCap, 2 kNmsCap) sorted
+    OutBox* const st = staging + (int64_t)f * 2 * kNmsCap;
+    if (n > kNmsCap) {
+        if (tid == 0) { atomicExch(&ctrl->nms_overflow, 1u); frame_counts[f] = 0; }
+    } else {
+        for (int i = tid; i < n; i += kNmsThreads) {
+            sm.parent[i] = i;
+            sm.sx[i] = sm.sy[i] = sm.sw[i] = sm.sh[i] = sm.cnt[i] = 0;
+            sm.best[i] = f2ord(-INFINITY);
+        }
+        __syncthreads();
+        // edges of the IoU >= 0.3 graph (every unordered pair once) -> union-find
+        for (int a = 0; a < n - 1; ++a) {
+            const short4 ba = sm.box[a];
+            for (int b = a + 1 + tid; b < n; b += kNmsThreads)
+                if (iou_edge(ba, sm.box[b])) unite(sm.parent, a, b);
+        }
+        __syncthreads();
+        for (int i = tid; i < n; i += kNmsThreads) {
+            const int r = find_root(sm.parent, i);
+            const short4 b = sm.box[i];
+            atomicAdd(&sm.sx[r], (int)b.x);
+            atomicAdd(&sm.sy[r], (int)b.y);
+            atomicAdd(&sm.sw[r], (int)b.z);
+            atomicAdd(&sm.sh[r], (int)b.w);
+            atomicAdd(&sm.cnt[r], 1);
+            atomicMax(&sm.best[r], f2ord(sm.score[i]));
+        }
+        __syncthreads();
+        for (int i = tid; i < n; i += kNmsThreads) {
+            if (sm.parent[i] != i || sm.cnt[i] < min_cluster) continue;
+            const int c = sm.cnt[i];
+            OutBox o;
+            o.frame = f;
+            o.x = (2 * sm.sx[i] + c) / (2 * c);
+            o.y = (2 * sm.sy[i] + c) / (2 * c);
+            o.w = (2 * sm.sw[i] + c) / (2 * c);
+            o.h = (2 * sm.sh[i] + c) / (2 * c);
+            o.score = ord2f(sm.best[i]);
+            o.neighbors = c;
+            st[atomicAdd(&sm.m, 1)] = o;
+        }
+        __syncthreads();
+        const int m = sm.m;
+        for (int i = tid; i < m; i += kNmsThreads) {             // rank sort
+            const OutBox a = st[i];
+            int r = 0;
+            for (int j = 0; j < m; ++j) r += before(st[j], j, a, i);
+            st[kNmsCap + r] = a;
+        }
+        if (tid == 0) frame_counts[f] = m;
+    }
+    // ---- the last CTA to finish compacts every frame's sorted result ----
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) sm.is_last = (atomicAdd(&ctrl->nms_done, 1u) == (uint32_t)(n_frames - 1));
+    __syncthreads();
+    if (!sm.is_last) return;
+    __threadfence();
+    int base = 0;
+    for (int g = 0; g < n_frames; ++g) {
+        const int c = *(volatile int32_t*)&frame_counts[g];
+        const OutBox* src = staging + (int64_t)g * 2 * kNmsCap + kNmsCap;
+        for (int k = tid; k < c; k += kNmsThreads) out[base + k] = src[k];
+        base += c;
+    }
+    if (tid == 0) ctrl->n_out = (uint32_t)base;
+}
+
+}  // namespace
+
+void launch_nms(const AccBox* acc, Ctrl* ctrl, int n_frames, int min_cluster, OutBox* staging,
+                int32_t* frame_counts, OutBox* out, cudaStream_t s)
+{
+    const size_t smem = sizeof(NmsSmem);
+    cudaFuncSetAttribute(nms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    nms_kernel<<<n_frames, kNmsThreads, smem, s>>>(acc, ctrl, n_frames, min_cluster, staging,
+                                                   frame_counts, out);
+}
+
+}  // namespace ccnn

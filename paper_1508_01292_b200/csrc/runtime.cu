@@ -1,0 +1,551 @@
+// runtime.cu -- host runtime behind the C ABI (include/ccnn.h): context, validation,
+// level planner, task table, device arena, launch sequence, readback, test hooks.
+//
+// Geometry (level table O1, pyramid sampling tables O2) is IEEE double evaluated in the
+// same operation order as PAPER.md's reading in DESIGN.md; this TU is compiled with
+// -ffp-contract=off so no multiply-add is fused and every value is bit-identical to
+// the oracle's independent implementation.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <algorithm>
+
+#include "../../include/ccnn.h"
+#include "ccnn_internal.h"
+
+using namespace ccnn;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t want)
+    {
+        if (want <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t grow = want + want / 4 + 4096;
+        cudaError_t e = cudaMalloc(&p, grow);
+        if (e == cudaSuccess) bytes = grow;
+        return e;
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct PlanKey {
+    int n = -1, W = -1, H = -1, min_face = -1;
+    float scale_step = 0.f;
+    bool operator==(const PlanKey& o) const
+    {
+        return n == o.n && W == o.W && H == o.H && min_face == o.min_face && scale_step == o.scale_step;
+    }
+};
+
+bool finite_all(const float* w, int64_t n)
+{
+    for (int64_t k = 0; k < n; ++k) if (!std::isfinite(w[k])) return false;
+    return true;
+}
+
+}  // namespace
+
+struct ccnn_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int debug = 0;
+
+    Cnn1W w1{};
+    Cnn2W w2{};
+    Cnn3W w3{};
+    float T1 = 0.f;
+    SelParams sp{};
+    int min_cluster = 1;
+    int max_w = 0, max_h = 0, max_batch = 0;
+    int queue_cap = 4096;
+    int seg_rows = 64;
+
+    // plan (cached per batch shape)
+    PlanKey key;
+    std::vector<LevelInfo> levels;
+    std::vector<S1Task> tasks;
+    std::vector<uint32_t> tabs;
+    int64_t level_frame_stride = 0;
+    int64_t map_frame_stride = 0;
+    int64_t windows_per_frame = 0;
+
+    DevBuf frames, arena, d_levels, d_tasks, d_tabs, cands, selout, dbg_resp, acc, ctrl, staging,
+        counts, out, dbg_map;
+    Ctrl* h_ctrl = nullptr;                 // pinned readback
+    cudaEvent_t ev[6] = {};
+
+    // last detect
+    int last_n = 0, last_W = 0, last_H = 0;
+    uint32_t last_cands = 0;
+    bool last_valid = false;
+};
+
+namespace {
+
+int fail(ccnn_ctx* c, int code, const std::string& msg)
+{
+    if (c) c->err = msg;
+    return code;
+}
+
+#define CU(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(ctx, CCNN_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// ---- architecture R check (include/ccnn.h CCNN_E_ARCH) ----
+bool layers_equal(const ccnn_net& n, const int (*ref)[5], int nl)
+{
+    if (n.n_layers != nl || !n.layers) return false;
+    for (int l = 0; l < nl; ++l) {
+        const ccnn_layer& L = n.layers[l];
+        if (L.kind != ref[l][0] || L.in_maps != ref[l][1] || L.out_maps != ref[l][2] ||
+            L.kw != ref[l][3] || L.kh != ref[l][4])
+            return false;
+    }
+    return true;
+}
+
+const int kR1[6][5] = {{0, 1, 6, 4, 4}, {1, 6, 6, 2, 2}, {0, 6, 6, 3, 3}, {1, 6, 6, 2, 2},
+                       {0, 6, 2, 5, 6}, {0, 2, 1, 1, 1}};
+const int kR2[6][5] = {{0, 1, 16, 4, 4}, {1, 16, 16, 2, 2}, {0, 16, 6, 3, 3}, {1, 6, 6, 2, 2},
+                       {0, 6, 2, 7, 8}, {0, 2, 1, 1, 1}};
+const int kR3[6][5] = {{0, 1, 2, 4, 4}, {1, 2, 2, 2, 2}, {0, 2, 2, 3, 3}, {1, 2, 2, 2, 2},
+                       {0, 2, 25, 7, 8}, {0, 25, 1, 1, 1}};
+
+int64_t conv_params(const int (*ref)[5], int nl)
+{
+    int64_t n = 0;
+    for (int l = 0; l < nl; ++l)
+        if (ref[l][0] == 0) n += (int64_t)ref[l][2] * (ref[l][1] * ref[l][3] * ref[l][4] + 1);
+    return n;
+}
+
+// The weight blob is [kernels][bias] per conv layer (S:186 order); our structs hold the
+// same values in the same order, so a straight copy per layer suffices.
+void unpack_cnn1(const float* w, Cnn1W& o)
+{
+    const float* p = w;
+    std::memcpy(o.w1, p, sizeof(o.w1)); p += 96;
+    std::memcpy(o.b1, p, sizeof(o.b1)); p += 6;
+    std::memcpy(o.w2, p, sizeof(o.w2)); p += 324;
+    std::memcpy(o.b2, p, sizeof(o.b2)); p += 6;
+    std::memcpy(o.w3, p, sizeof(o.w3)); p += 360;
+    std::memcpy(o.b3, p, sizeof(o.b3)); p += 2;
+    std::memcpy(o.w4, p, sizeof(o.w4)); p += 2;
+    o.b4 = *p;
+}
+template <int A, int B, int C>
+void unpack_sel(const float* p, SelNetW<A, B, C>& o)
+{
+    std::memcpy(o.w1, p, sizeof(o.w1)); p += A * 16;
+    std::memcpy(o.b1, p, sizeof(o.b1)); p += A;
+    std::memcpy(o.w2, p, sizeof(o.w2)); p += B * A * 9;
+    std::memcpy(o.b2, p, sizeof(o.b2)); p += B;
+    std::memcpy(o.w3, p, sizeof(o.w3)); p += C * B * 56;
+    std::memcpy(o.b3, p, sizeof(o.b3)); p += C;
+    std::memcpy(o.w4, p, sizeof(o.w4)); p += C;
+    o.b4 = *p;
+}
+
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// O2 sampling table entry: s = (d + 0.5)/sigma - 0.5, clamp [0, n-1], i0 = floor(s),
+// a = floor((s - i0) * 2048 + 0.5); packed i0 | a << 16.
+uint32_t sample_entry(int d, double sigma, int n)
+{
+    double s = ((double)d + 0.5) / sigma - 0.5;
+    if (s < 0.0) s = 0.0;
+    if (s > (double)(n - 1)) s = (double)(n - 1);
+    const int f = (int)std::floor(s);
+    const int a = (int)std::floor((s - (double)f) * 2048.0 + 0.5);
+    return (uint32_t)f | ((uint32_t)a << 16);
+}
+
+// Level table O1 + stage-1 task table + sampling tables for one batch shape.
+void build_plan(ccnn_ctx* c, int n, int W, int H, int min_face, float scale_step)
+{
+    c->levels.clear();
+    c->tasks.clear();
+    c->tabs.clear();
+    const double sf = (double)scale_step;
+    double s = (double)kWinW / (double)min_face;
+    int64_t off = 0, map_off = 0;
+    int row0 = 0;
+    c->windows_per_frame = 0;
+    while (true) {
+        const int lw = (int)std::floor((double)W * s);
+        const int lh = (int)std::floor((double)H * s);
+        if (lw < kWinW || lh < kWinH) break;
+        LevelInfo L{};
+        L.sigma = s;
+        L.lw = lw;
+        L.lh = lh;
+        L.pitch = (int)round_up(lw, 16);
+        L.offset = off;
+        L.nx = (lw - kWinW) / kStep + 1;
+        L.ny = (lh - kWinH) / kStep + 1;
+        L.map_off = (int32_t)map_off;
+        L.tab_off = (int32_t)c->tabs.size();
+        L.row0 = row0;
+        for (int x = 0; x < lw; ++x) c->tabs.push_back(sample_entry(x, s, W));
+        for (int y = 0; y < lh; ++y) c->tabs.push_back(sample_entry(y, s, H));
+        off += round_up((int64_t)L.pitch * lh, 256);
+        map_off += (int64_t)L.nx * L.ny;
+        row0 += lh;
+        c->windows_per_frame += (int64_t)L.nx * L.ny;
+        c->levels.push_back(L);
+        s = s / sf;
+    }
+    // slack so that the stage-1 loader's last (clamped) word read stays in bounds
+    c->level_frame_stride = round_up(off + 256, 256);
+    c->map_frame_stride = map_off;
+    const int TW = stage1_band_width();
+    std::vector<S1Task> one;
+    for (int l = 0; l < (int)c->levels.size(); ++l) {
+        const LevelInfo& L = c->levels[l];
+        const int nseg = std::max(1, (L.ny + c->seg_rows - 1) / c->seg_rows);
+        const int rows = (L.ny + nseg - 1) / nseg;
+        for (int x0 = 0; x0 < L.nx; x0 += TW)
+            for (int y0 = 0; y0 < L.ny; y0 += rows) {
+                S1Task t{};
+                t.level = (int16_t)l;
+                t.bw = (int16_t)std::min(TW, L.nx - x0);
+                t.x0 = (int16_t)x0;
+                t.y0 = (int16_t)y0;
+                t.nrows = (int16_t)std::min(rows, L.ny - y0);
+                one.push_back(t);
+            }
+    }
+    // longest tasks first (cost ~ nrows + 8 steps regardless of band width), frames interleaved
+    std::stable_sort(one.begin(), one.end(),
+                     [](const S1Task& a, const S1Task& b) { return a.nrows > b.nrows; });
+    c->tasks.reserve(one.size() * n);
+    for (const S1Task& t : one)
+        for (int f = 0; f < n; ++f) {
+            S1Task u = t;
+            u.frame = f;
+            c->tasks.push_back(u);
+        }
+}
+
+}  // namespace
+
+extern "C" {
+
+int ccnn_abi_version(void) { return CCNN_ABI_VERSION; }
+
+const char* ccnn_last_error(const ccnn_ctx* ctx)
+{
+    if (!ctx) return "ccnn: NULL context (ccnn_create failed or was not called)";
+    return ctx->err.c_str();
+}
+
+int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
+{
+    ccnn_ctx* ctx = nullptr;
+    if (!p || !out) return CCNN_E_ARG;
+    if (!layers_equal(p->net[0], kR1, 6) || !layers_equal(p->net[1], kR2, 6) ||
+        !layers_equal(p->net[2], kR3, 6))
+        return CCNN_E_ARCH;
+    if (p->net[0].n_weights != conv_params(kR1, 6) || p->net[1].n_weights != conv_params(kR2, 6) ||
+        p->net[2].n_weights != conv_params(kR3, 6))
+        return CCNN_E_WEIGHTS;
+    for (int k = 0; k < 3; ++k)
+        if (!p->net[k].weights || !finite_all(p->net[k].weights, p->net[k].n_weights)) return CCNN_E_WEIGHTS;
+    if (!std::isfinite(p->T1) || !std::isfinite(p->T2[0]) || !std::isfinite(p->T2[1])) return CCNN_E_WEIGHTS;
+    if (p->Tnn < 1 || (p->rule != 0 && p->rule != 1) || p->max_w < kWinW || p->max_h < kWinH ||
+        p->max_w > 16384 || p->max_h > 16384 || p->max_batch < 1 || p->queue_capacity < 0 ||
+        p->nms_min_cluster < 0 || p->segment_rows < 0)
+        return CCNN_E_ARG;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev)
+        return CCNN_E_CUDA;
+    ctx = new ccnn_ctx();
+    ctx->device = cuda_device;
+    CU(cudaSetDevice(cuda_device));
+    CU(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, cuda_device));
+    unpack_cnn1(p->net[0].weights, ctx->w1);
+    unpack_sel(p->net[1].weights, ctx->w2);
+    unpack_sel(p->net[2].weights, ctx->w3);
+    ctx->T1 = p->T1;
+    ctx->sp.T2a = p->T2[0];
+    ctx->sp.T2b = p->T2[1];
+    ctx->sp.Tnn = p->Tnn;
+    ctx->sp.rule = p->rule;
+    ctx->min_cluster = p->nms_min_cluster < 1 ? 1 : p->nms_min_cluster;
+    ctx->max_w = p->max_w;
+    ctx->max_h = p->max_h;
+    ctx->max_batch = p->max_batch;
+    ctx->queue_cap = p->queue_capacity > 0 ? p->queue_capacity : 4096;
+    ctx->seg_rows = p->segment_rows > 0 ? p->segment_rows : 64;
+    CU(cudaMallocHost(&ctx->h_ctrl, sizeof(Ctrl)));
+    for (auto& e : ctx->ev) CU(cudaEventCreate(&e));
+    CU(ctx->ctrl.ensure(sizeof(Ctrl)));
+    *out = ctx;
+    return CCNN_OK;
+}
+
+int ccnn_set_stream(ccnn_ctx* ctx, void* cuda_stream)
+{
+    if (!ctx) return CCNN_E_ARG;
+    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+    return CCNN_OK;
+}
+
+int ccnn_set_debug(ccnn_ctx* ctx, int flags)
+{
+    if (!ctx) return CCNN_E_ARG;
+    ctx->debug = flags;
+    return CCNN_OK;
+}
+
+void ccnn_destroy(ccnn_ctx* ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream); else cudaDeviceSynchronize();
+    for (DevBuf* b : {&ctx->frames, &ctx->arena, &ctx->d_levels, &ctx->d_tasks, &ctx->d_tabs,
+                      &ctx->cands, &ctx->selout, &ctx->dbg_resp, &ctx->acc, &ctx->ctrl,
+                      &ctx->staging, &ctx->counts, &ctx->out, &ctx->dbg_map})
+        b->release();
+    if (ctx->h_ctrl) cudaFreeHost(ctx->h_ctrl);
+    for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
+    delete ctx;
+}
+
+int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64_t pitch,
+                int frames_on_device, int min_face, float scale_step, ccnn_box* boxes,
+                int64_t box_cap, int64_t* n_boxes, ccnn_stats* stats)
+{
+    if (!ctx) return CCNN_E_ARG;
+    ctx->last_valid = false;
+    if (!frames || !n_boxes || (box_cap > 0 && !boxes))
+        return fail(ctx, CCNN_E_ARG, "NULL frames / n_boxes / boxes");
+    if (n <= 0 || n > ctx->max_batch) return fail(ctx, CCNN_E_ARG, "n out of [1, max_batch]");
+    if (w < 1 || h < 1 || w > ctx->max_w || h > ctx->max_h)
+        return fail(ctx, CCNN_E_ARG, "frame size out of [1, max_w] x [1, max_h]");
+    if (pitch < w) return fail(ctx, CCNN_E_ARG, "pitch < width");
+    if (min_face < 1) return fail(ctx, CCNN_E_ARG, "min_face < 1");
+    if (!(scale_step > 1.0f) || !std::isfinite(scale_step))
+        return fail(ctx, CCNN_E_ARG, "scale_step must be > 1 (S:227)");
+    if ((double)kWinW / min_face * std::max(w, h) > 32000.0)
+        return fail(ctx, CCNN_E_ARG, "level 0 too large (min_face too small for this frame)");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const bool timing = stats != nullptr;
+
+    PlanKey key{n, w, h, min_face, scale_step};
+    const bool replan = !(key == ctx->key);
+    if (replan) build_plan(ctx, n, w, h, min_face, scale_step);
+    const int L = (int)ctx->levels.size();
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->windows = ctx->windows_per_frame * n;
+    }
+    ctx->last_n = n;
+    ctx->last_W = w;
+    ctx->last_H = h;
+    if (L == 0) {                                  // empty pyramid: not an error
+        *n_boxes = 0;
+        ctx->key = key;
+        ctx->last_cands = 0;
+        ctx->last_valid = true;
+        return CCNN_OK;
+    }
+
+    const uint32_t cand_cap = (uint32_t)std::min<int64_t>((int64_t)ctx->queue_cap * n, 0x7FFFFFFF);
+    CU(ctx->arena.ensure((size_t)ctx->level_frame_stride * n));
+    CU(ctx->d_levels.ensure(sizeof(LevelInfo) * L));
+    CU(ctx->d_tasks.ensure(sizeof(S1Task) * ctx->tasks.size()));
+    CU(ctx->d_tabs.ensure(sizeof(uint32_t) * ctx->tabs.size()));
+    CU(ctx->cands.ensure(sizeof(S1Cand) * cand_cap));
+    CU(ctx->selout.ensure(sizeof(SelOut) * cand_cap));
+    CU(ctx->acc.ensure(sizeof(AccBox) * cand_cap));
+    CU(ctx->staging.ensure(sizeof(OutBox) * 2 * kNmsCap * (size_t)n));
+    CU(ctx->counts.ensure(sizeof(int32_t) * n));
+    CU(ctx->out.ensure(sizeof(OutBox) * cand_cap));
+    const bool dbg1 = (ctx->debug & CCNN_DEBUG_STAGE1) != 0;
+    if (dbg1) {
+        CU(ctx->dbg_map.ensure(sizeof(float) * ctx->map_frame_stride * n));
+        CU(ctx->dbg_resp.ensure(sizeof(float) * 100 * (size_t)cand_cap));
+    }
+    if (replan || ctx->key.n < 0) {
+        CU(cudaMemcpyAsync(ctx->d_levels.p, ctx->levels.data(), sizeof(LevelInfo) * L,
+                           cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(ctx->d_tasks.p, ctx->tasks.data(), sizeof(S1Task) * ctx->tasks.size(),
+                           cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(ctx->d_tabs.p, ctx->tabs.data(), sizeof(uint32_t) * ctx->tabs.size(),
+                           cudaMemcpyHostToDevice, s));
+        CU(cudaStreamSynchronize(s));   // host vectors may change on the next replan
+    }
+    ctx->key = key;
+
+    // ---- frames: device-resident, or H2D into the ctx buffer (host -> device boundary) ----
+    const uint8_t* dframes = frames;
+    int64_t dpitch = pitch;
+    if (timing) CU(cudaEventRecord(ctx->ev[0], s));
+    if (!frames_on_device) {
+        dpitch = round_up(w, 16);
+        CU(ctx->frames.ensure((size_t)dpitch * h * n));
+        CU(cudaMemcpy2DAsync(ctx->frames.p, dpitch, frames, pitch, w, (size_t)h * n,
+                             cudaMemcpyHostToDevice, s));
+        dframes = ctx->frames.as<uint8_t>();
+    }
+    const int64_t fstride = dpitch * h;
+    CU(cudaMemsetAsync(ctx->ctrl.p, 0, sizeof(Ctrl), s));
+    if (timing) CU(cudaEventRecord(ctx->ev[1], s));
+    launch_pyramid(dframes, fstride, dpitch, w, h, ctx->arena.as<uint8_t>(), ctx->level_frame_stride,
+                   ctx->d_levels.as<LevelInfo>(), ctx->levels.data(), L, ctx->d_tabs.as<uint32_t>(), n, s);
+    if (timing) CU(cudaEventRecord(ctx->ev[2], s));
+    launch_stage1(ctx->w1, ctx->T1, ctx->arena.as<uint8_t>(), ctx->level_frame_stride,
+                  ctx->d_levels.as<LevelInfo>(), ctx->d_tasks.as<S1Task>(), (int)ctx->tasks.size(),
+                  ctx->cands.as<S1Cand>(), cand_cap, ctx->ctrl.as<Ctrl>(),
+                  dbg1 ? ctx->dbg_map.as<float>() : nullptr, ctx->map_frame_stride, ctx->sm_count, s);
+    if (timing) CU(cudaEventRecord(ctx->ev[3], s));
+    launch_selective(ctx->w2, ctx->w3, ctx->sp, dframes, fstride, dpitch, w, h,
+                     ctx->d_levels.as<LevelInfo>(), ctx->cands.as<S1Cand>(), cand_cap,
+                     ctx->selout.as<SelOut>(), dbg1 ? ctx->dbg_resp.as<float>() : nullptr,
+                     ctx->acc.as<AccBox>(), ctx->ctrl.as<Ctrl>(), ctx->sm_count, s);
+    if (timing) CU(cudaEventRecord(ctx->ev[4], s));
+    launch_nms(ctx->acc.as<AccBox>(), ctx->ctrl.as<Ctrl>(), n, ctx->min_cluster,
+               ctx->staging.as<OutBox>(), ctx->counts.as<int32_t>(), ctx->out.as<OutBox>(), s);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(ctx->h_ctrl, ctx->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    if (timing) CU(cudaEventRecord(ctx->ev[5], s));
+    CU(cudaStreamSynchronize(s));
+    const Ctrl& hc = *ctx->h_ctrl;
+    ctx->last_cands = hc.n_cand;
+    if (hc.n_cand > cand_cap)
+        return fail(ctx, CCNN_E_QUEUE, "stage-1 survivor queue overflow: " + std::to_string(hc.n_cand) +
+                                           " > capacity " + std::to_string(cand_cap));
+    if (hc.nms_overflow)
+        return fail(ctx, CCNN_E_QUEUE, "more than 4096 accepted regions in one frame");
+    ctx->last_valid = true;
+    if (stats) {
+        stats->stage1 = hc.n_cand;
+        stats->stage2 = hc.n_stage2;
+        stats->stage3 = hc.n_stage3;
+        stats->nms = hc.n_out;
+        stats->kernel_launches = 4;
+        float t;
+        for (int k = 0; k < 5; ++k) {
+            cudaEventElapsedTime(&t, ctx->ev[k], ctx->ev[k + 1]);
+            stats->ms[k] = t;
+        }
+    }
+    *n_boxes = hc.n_out;
+    if ((int64_t)hc.n_out > box_cap)
+        return fail(ctx, CCNN_E_CAPACITY, "box_cap too small: need " + std::to_string(hc.n_out));
+    if (hc.n_out) {
+        static_assert(sizeof(OutBox) == sizeof(ccnn_box), "OutBox mirrors ccnn_box");
+        CU(cudaMemcpyAsync(boxes, ctx->out.p, sizeof(OutBox) * hc.n_out, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+    }
+    return CCNN_OK;
+}
+
+int ccnn_debug_levels(ccnn_ctx* ctx, double* sigma, int32_t* lw, int32_t* lh, int cap)
+{
+    if (!ctx) return CCNN_E_ARG;
+    const int L = (int)ctx->levels.size();
+    for (int l = 0; l < L && l < cap; ++l) {
+        if (sigma) sigma[l] = ctx->levels[l].sigma;
+        if (lw) lw[l] = ctx->levels[l].lw;
+        if (lh) lh[l] = ctx->levels[l].lh;
+    }
+    return L;
+}
+
+int ccnn_debug_level(ccnn_ctx* ctx, int frame, int level, uint8_t* out, int64_t cap)
+{
+    if (!ctx || !out) return CCNN_E_ARG;
+    if (!ctx->last_valid) return fail(ctx, CCNN_E_STATE, "no completed detect");
+    if (frame < 0 || frame >= ctx->last_n || level < 0 || level >= (int)ctx->levels.size())
+        return fail(ctx, CCNN_E_ARG, "frame/level out of range");
+    const LevelInfo& L = ctx->levels[level];
+    if (cap < (int64_t)L.lw * L.lh) return fail(ctx, CCNN_E_CAPACITY, "cap < lw*lh");
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaMemcpy2DAsync(out, L.lw, ctx->arena.as<uint8_t>() + frame * ctx->level_frame_stride + L.offset,
+                         L.pitch, L.lw, L.lh, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return CCNN_OK;
+}
+
+int ccnn_debug_stage1_map(ccnn_ctx* ctx, int frame, int level, float* out, int64_t cap)
+{
+    if (!ctx || !out) return CCNN_E_ARG;
+    if (!ctx->last_valid || !(ctx->debug & CCNN_DEBUG_STAGE1))
+        return fail(ctx, CCNN_E_STATE, "needs CCNN_DEBUG_STAGE1 before ccnn_detect");
+    if (frame < 0 || frame >= ctx->last_n || level < 0 || level >= (int)ctx->levels.size())
+        return fail(ctx, CCNN_E_ARG, "frame/level out of range");
+    const LevelInfo& L = ctx->levels[level];
+    const int64_t cnt = (int64_t)L.nx * L.ny;
+    if (cap < cnt) return fail(ctx, CCNN_E_CAPACITY, "cap < nx*ny");
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaMemcpyAsync(out, ctx->dbg_map.as<float>() + frame * ctx->map_frame_stride + L.map_off,
+                       sizeof(float) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return CCNN_OK;
+}
+
+int ccnn_debug_candidates(ccnn_ctx* ctx, ccnn_candidate* out, int64_t cap, int64_t* n)
+{
+    if (!ctx || !n) return CCNN_E_ARG;
+    if (!ctx->last_valid) return fail(ctx, CCNN_E_STATE, "no completed detect");
+    const int64_t cnt = ctx->last_cands;
+    *n = cnt;
+    if (cnt == 0) return CCNN_OK;
+    if (!out || cap < cnt) return fail(ctx, CCNN_E_CAPACITY, "cap < candidate count");
+    CU(cudaSetDevice(ctx->device));
+    std::vector<S1Cand> c(cnt);
+    std::vector<SelOut> so(cnt);
+    std::vector<float> resp;
+    CU(cudaMemcpyAsync(c.data(), ctx->cands.p, sizeof(S1Cand) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(so.data(), ctx->selout.p, sizeof(SelOut) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    const bool have_resp = (ctx->debug & CCNN_DEBUG_STAGE1) && ctx->dbg_resp.p;
+    if (have_resp) {
+        resp.resize((size_t)cnt * 100);
+        CU(cudaMemcpyAsync(resp.data(), ctx->dbg_resp.p, sizeof(float) * 100 * cnt,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int64_t k = 0; k < cnt; ++k) {
+        ccnn_candidate& o = out[k];
+        std::memset(&o, 0, sizeof(o));
+        o.frame = c[k].frame;
+        o.level = c[k].level;
+        o.ix = c[k].ix;
+        o.iy = c[k].iy;
+        o.s1 = c[k].s1;
+        o.K2 = so[k].K2;
+        o.K3 = so[k].K3;
+        o.delta = so[k].delta;
+        o.cnn3_ran = so[k].cnn3_ran;
+        o.score = so[k].score;
+        o.bx = so[k].bx;
+        o.by = so[k].by;
+        o.bw = so[k].bw;
+        o.bh = so[k].bh;
+        if (have_resp) {
+            std::memcpy(o.r2, &resp[k * 100], sizeof(o.r2));
+            std::memcpy(o.r3, &resp[k * 100 + 50], sizeof(o.r3));
+        }
+    }
+    return CCNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,222 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle, element by element.
+
+Sizes the oracle finishes in seconds that still span several stage-1 bands/segments and
+ragged tails, plus BASELINE.json's full 4K size in the bench's launch configuration on
+sampled outputs.  Tolerances: tests/parity.py (1e-4 absolute on scores, exact elsewhere).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth import arch, configs, frames as synth_frames, weights
+
+from . import parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ws():
+    return weights.make_cascade_weights()
+
+
+def make_det(ws, T1, T2, Tnn=2, rule=0, **kw):
+    from paper_1508_01292_b200 import Detector
+    args = dict(max_w=3840, max_h=2160, max_batch=32, queue_capacity=4096)
+    args.update(kw)
+    return Detector(arch.NETS, ws, T1, T2, Tnn, rule, **args)
+
+
+def quantile_T1(cascade, frames, min_face, sf, q):
+    lv, maps = parity.oracle_maps(cascade, frames, min_face, sf)
+    allv = np.concatenate([m.ravel() for m in maps.values()])
+    return float(np.float32(np.quantile(allv, q)))
+
+
+def test_c1_parity_calibrated(ws, cascade):
+    c = configs.C1
+    T1, T2 = c.thresholds()
+    fr = c.make_frames()
+    det = make_det(ws, T1, T2, c.Tnn, c.rule)
+    rep = parity.compare_run(det, cascade, fr, c.min_face, c.scale_step, T1, T2, c.Tnn, c.rule)
+    print(rep)
+
+
+@pytest.mark.parametrize("rule", [0, 1])
+def test_c1_parity_low_threshold(ws, cascade, rule):
+    """T1 at the 97% quantile so ~400 windows reach the selective unit."""
+    c = configs.C1
+    fr = c.make_frames()
+    T1 = quantile_T1(cascade, fr, c.min_face, c.scale_step, 0.97)
+    T2 = (0.9, 0.2)
+    det = make_det(ws, T1, T2, 2, rule)
+    rep = parity.compare_run(det, cascade, fr, c.min_face, c.scale_step, T1, T2, 2, rule)
+    assert rep["survivors"] > 200
+    print(rep)
+
+
+def test_ragged_multi_frame_batch(ws, cascade):
+    """odd sizes, upscaled level 0 (min_face < 27), scale 1.1, several frames per call."""
+    fr = synth_frames.make_stills(3, 333, 257, 991, 20)
+    T1 = quantile_T1(cascade, fr, 20, 1.1, 0.995)
+    T2 = (0.8, 0.1)
+    det = make_det(ws, T1, T2, 1, 0)
+    rep = parity.compare_run(det, cascade, fr, 20, 1.1, T1, T2, 1, 0)
+    print(rep)
+
+
+def test_fddb_like_stills(ws, cascade):
+    """C2 settings (minSize 15, scaleFactor 1.05: 67 levels) on 2 of the 450x450 stills."""
+    c = configs.C2
+    fr = c.make_frames(2)
+    T1 = quantile_T1(cascade, fr, c.min_face, c.scale_step, 0.9995)
+    T2 = (0.9, 0.2)
+    det = make_det(ws, T1, T2, c.Tnn, c.rule)
+    rep = parity.compare_run(det, cascade, fr, c.min_face, c.scale_step, T1, T2, c.Tnn, c.rule,
+                             check_levels=True)
+    print(rep)
+
+
+def test_c4_full_size_bench_config(ws, cascade):
+    """4K, min face 60, the bench's batch and launch configuration (production kernel, no
+    debug map): every survivor vs the per-window oracle, sampled windows one by one vs the
+    survivor set, and full oracle boxes on 2 frames."""
+    c = configs.C4
+    T1, T2 = c.thresholds()
+    fr = c.make_frames()
+    det = make_det(ws, T1, T2, c.Tnn, c.rule)
+    boxes = det.detect(fr, c.min_face, c.scale_step)
+    st = det.last_stats
+    cands = det.candidates()
+    lv = oracle.level_table(c.width, c.height, c.min_face, c.scale_step)
+    assert st["windows"] == len(fr) * sum(oracle.window_grid(w, h)[0] * oracle.window_grid(w, h)[1]
+                                          for _, w, h in lv)
+    assert st["stage1"] == len(cands) > 0
+    rng = np.random.default_rng(1)
+    gset = {parity.key(x) for x in cands}
+    # every survivor: per-window oracle score within 1e-4 and above T1 - 1e-4
+    lev_cache = {}
+
+    def level(f, l):
+        if (f, l) not in lev_cache:
+            s, w, h = lv[l]
+            lev_cache[(f, l)] = oracle.resample(fr[f], s, w, h)
+        return lev_cache[(f, l)]
+    for x in cands:
+        f, l, i, j = parity.key(x)
+        s1 = oracle.stage1_window(cascade.nets[0], level(f, l), i, j)
+        assert abs(float(x["s1"]) - s1) <= parity.TOL
+        assert s1 > T1 - parity.TOL
+    # sampled windows (uniform over frames x levels x positions) vs the survivor set
+    n_checked = 0
+    for _ in range(3000):
+        f = int(rng.integers(len(fr)))
+        l = int(rng.integers(len(lv)))
+        nx, ny = oracle.window_grid(lv[l][1], lv[l][2])
+        i, j = int(rng.integers(ny)), int(rng.integers(nx))
+        s1 = oracle.stage1_window(cascade.nets[0], level(f, l), i, j)
+        if abs(s1 - T1) <= parity.TOL:
+            continue
+        assert ((f, l, i, j) in gset) == (np.float32(s1) > np.float32(T1))
+        n_checked += 1
+    assert n_checked > 2900
+    # near-threshold windows must be the only possible disagreements: full oracle on 2 frames
+    for f in (0, len(fr) - 1):
+        oc, ob, os_ = oracle.detect(cascade, fr[f:f + 1], c.min_face, c.scale_step, T1, T2, c.Tnn,
+                                    c.rule)
+        oset = {(f, int(k["level"]), int(k["iy"]), int(k["ix"])) for k in oc}
+        gf = {k for k in gset if k[0] == f}
+        diff = oset ^ gf
+        for (_, l, i, j) in diff:
+            s1 = oracle.stage1_window(cascade.nets[0], level(f, l), i, j)
+            assert abs(s1 - T1) <= parity.TOL
+        if not diff and not any(np.any(np.abs(k["r2"] - T2[0]) <= parity.TOL) or
+                                np.any(np.abs(k["r3"] - T2[1]) <= parity.TOL) for k in oc):
+            gb = sorted((int(b["x"]), int(b["y"]), int(b["w"]), int(b["h"]), int(b["neighbors"]))
+                        for b in boxes[boxes["frame"] == f])
+            obx = sorted((int(b["x"]), int(b["y"]), int(b["w"]), int(b["h"]), int(b["neighbors"]))
+                         for b in ob)
+            assert gb == obx
+
+
+def test_c4_debug_map_sampled(ws, cascade):
+    """Dense stage-1 map of a 4K frame (debug instantiation) at 4000 sampled windows."""
+    c = configs.C4
+    T1, T2 = c.thresholds()
+    fr = c.make_frames(2)
+    det = make_det(ws, T1, T2, c.Tnn, c.rule)
+    from paper_1508_01292_b200 import ccnn
+    det.set_debug(ccnn.CCNN_DEBUG_STAGE1)
+    det.detect(fr, c.min_face, c.scale_step)
+    lv = oracle.level_table(c.width, c.height, c.min_face, c.scale_step)
+    rng = np.random.default_rng(2)
+    worst = 0.0
+    for f in range(2):
+        for l, (s, w, h) in enumerate(lv):
+            L = oracle.resample(fr[f], s, w, h)
+            assert np.array_equal(det.level_image(f, l), L)
+            m = det.stage1_map(f, l)
+            ny, nx = m.shape
+            for _ in range(100):
+                i, j = int(rng.integers(ny)), int(rng.integers(nx))
+                d = abs(float(m[i, j]) - oracle.stage1_window(cascade.nets[0], L, i, j))
+                worst = max(worst, d)
+            # the last row and column of windows (ragged band / segment tails)
+            for i, j in [(ny - 1, nx - 1), (0, nx - 1), (ny - 1, 0)]:
+                d = abs(float(m[i, j]) - oracle.stage1_window(cascade.nets[0], L, i, j))
+                worst = max(worst, d)
+    assert worst <= parity.TOL, worst
+
+
+def test_edge_cases(ws, cascade):
+    from paper_1508_01292_b200 import ccnn
+    det = make_det(ws, 0.5, (0.5, 0.5), max_w=640, max_h=480, max_batch=4, queue_capacity=64)
+    # empty pyramid (frame smaller than the window at every scale): no boxes, not an error
+    b = det.detect(np.zeros((1, 30, 26), np.uint8), 27, 1.2)
+    assert len(b) == 0 and det.last_stats["windows"] == 0
+    # exactly one window
+    fr = synth_frames.make_still(27, 31, 5, 27)[None]
+    det.detect(fr, 27, 1.2)
+    assert det.last_stats["windows"] == 1
+    # invalid arguments
+    for args in [(np.zeros((1, 100, 100), np.uint8), 0, 1.2), (np.zeros((1, 100, 100), np.uint8), 24, 1.0),
+                 (np.zeros((1, 500, 700), np.uint8), 24, 1.2), (np.zeros((5, 100, 100), np.uint8), 24, 1.2)]:
+        with pytest.raises(ccnn.CcnnError) as e:
+            det.detect(*args)
+        assert e.value.code == ccnn.CCNN_E_ARG
+    # survivor queue overflow is an error, never silent
+    low = make_det(ws, -1.8, (0.5, 0.5), max_w=640, max_h=480, max_batch=2, queue_capacity=16)
+    with pytest.raises(ccnn.CcnnError) as e:
+        low.detect(configs.C1.make_frames(), 24, 1.2)
+    assert e.value.code == ccnn.CCNN_E_QUEUE
+    # box capacity retry semantics
+    c = configs.C1
+    fr = c.make_frames()
+    T1 = quantile_T1(cascade, fr, c.min_face, c.scale_step, 0.97)
+    d2 = make_det(ws, T1, (0.9, 0.2), max_w=640, max_h=480, max_batch=4)
+    full = d2.detect(fr, c.min_face, c.scale_step)
+    assert len(full) >= 1
+    with pytest.raises(ccnn.CcnnError) as e:
+        d2.detect(fr, c.min_face, c.scale_step, box_cap=0)
+    assert e.value.code == ccnn.CCNN_E_CAPACITY
+
+
+def test_host_vs_device_frames_and_determinism(ws):
+    import torch
+    c = configs.C3
+    T1, T2 = c.thresholds()
+    fr = c.make_frames(4)
+    det = make_det(ws, T1, T2, c.Tnn, c.rule)
+    a = det.detect(fr, c.min_face, c.scale_step)
+    pinned = torch.from_numpy(fr).pin_memory()
+    b = det.detect(pinned, c.min_face, c.scale_step)
+    dev = torch.from_numpy(fr).cuda()
+    d = det.detect(dev, c.min_face, c.scale_step)
+    e = det.detect(dev, c.min_face, c.scale_step)
+    for x in (b, d, e):
+        assert np.array_equal(a, x)
+    # a pitched (strided-row) device batch
+    big = torch.zeros((4, c.height, c.width + 64), dtype=torch.uint8, device="cuda")
+    big[:, :, :c.width] = dev
+    f = det.detect(big[:, :, :c.width], c.min_face, c.scale_step)
+    assert np.array_equal(a, f)
