@@ -171,6 +171,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="frames per step per GPU (0 = config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--seg", type=int, default=0, help="stage-1 segment rows (0 = adaptive)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -201,7 +202,7 @@ def main():
     frames = cfg.make_frames(batch, seed=configs.FRAME_SEED + 7919 * rank)
     det = Detector(arch.NETS, ws, T1, T2, cfg.Tnn, cfg.rule, max_w=cfg.width, max_h=cfg.height,
                    max_batch=batch, queue_capacity=max(4096, 40000 if cfg.kind == "clutter" else 0),
-                   device=dev.index)
+                   segment_rows=args.seg, device=dev.index)
     stream = torch.cuda.current_stream(dev)
     det.set_stream(stream.cuda_stream)
     dframes = torch.from_numpy(frames).to(dev)
@@ -315,8 +316,6 @@ def main():
         }
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(cfg, ws, frames, T1, T2)
-        elif not args.no_cpu_baseline:
-            line["cpu_baseline"] = None
         print(json.dumps(line), flush=True)
     det.close()
     if dist is not None:

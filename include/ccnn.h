@@ -78,7 +78,7 @@ typedef struct {
     int32_t max_w, max_h;      /* largest frame accepted by ccnn_detect                        */
     int32_t max_batch;         /* largest n accepted by ccnn_detect                            */
     int32_t queue_capacity;    /* stage-1 survivor records per frame (S:430 default 4096)     */
-    int32_t segment_rows;      /* stage-1 task height in window rows (0 = default 64)         */
+    int32_t segment_rows;      /* stage-1 task height in window rows (0 = adaptive)            */
 } ccnn_params;
 
 /* A resulting face area in original-image pixels. */
@@ -161,7 +161,12 @@ typedef struct {
     int32_t bx, by, bw, bh;        /* raw box (O8) */
 } ccnn_candidate;
 
-/* Copy the survivors of the last detect (unordered), *n = total count. */
+/* Device profiling counters of the last detect (kernel-build dependent; zeros unless
+ * built with -DS1_PROFILE): up to cap words into out, returns the count. */
+int ccnn_debug_counters(ccnn_ctx* ctx, uint32_t* out, int cap);
+
+/* Copy the survivors of the last detect (unordered), *n = total count; out == NULL only
+ * queries the count. */
 int ccnn_debug_candidates(ccnn_ctx* ctx, ccnn_candidate* out, int64_t cap, int64_t* n);
 
 #ifdef __cplusplus

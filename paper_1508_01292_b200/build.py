@@ -24,20 +24,33 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, variant=None, defines=()):
+    """variant: build libccnn_<variant>.so with extra -D defines (experiments only)."""
+    global LIB
+    if variant:
+        saved = LIB
+        LIB = os.path.join(PKG, "libccnn_%s.so" % variant)
+        try:
+            return _build(True, verbose, ["-D" + d for d in defines], "build_" + variant)
+        finally:
+            LIB = saved
+    return _build(force, verbose, [], "build")
+
+
+def _build(force, verbose, extra, objname):
     srcs = sources()
     deps = srcs + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "ccnn.h"),
                                                           __file__]
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(map(os.path.getmtime, deps)):
         return LIB
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, objname)
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for s in srcs:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
         objs.append(o)
-        cmd = [NVCC] + NVCC_FLAGS + ["-c", s, "-o", o]
+        cmd = [NVCC] + NVCC_FLAGS + extra + ["-c", s, "-o", o]
         procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     logs = []
     for s, p in procs:
@@ -58,4 +71,8 @@ def build(force=False, verbose=False):
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    if args:   # python build.py <variant> DEFINE1 DEFINE2 ...
+        build(variant=args[0], defines=args[1:])
+    else:
+        build(force="--force" in sys.argv, verbose=True)

@@ -11,6 +11,8 @@ import os
 import numpy as np
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libccnn.so")
+if os.environ.get("CCNN_LIB_VARIANT"):      # experiments only: an in-tree variant build
+    LIB_PATH = os.path.join(os.path.dirname(LIB_PATH), "libccnn_%s.so" % os.environ["CCNN_LIB_VARIANT"])
 
 CCNN_OK, CCNN_E_ARG, CCNN_E_ARCH, CCNN_E_WEIGHTS = 0, -1, -2, -3
 CCNN_E_CAPACITY, CCNN_E_QUEUE, CCNN_E_CUDA, CCNN_E_STATE = -4, -5, -6, -7
@@ -19,7 +21,7 @@ CCNN_DEBUG_LEVELS, CCNN_DEBUG_STAGE1 = 1, 2
 # every entry point declared in include/ccnn.h
 EXPORTS = ("ccnn_create", "ccnn_set_stream", "ccnn_detect", "ccnn_destroy", "ccnn_last_error",
            "ccnn_abi_version", "ccnn_set_debug", "ccnn_debug_levels", "ccnn_debug_level",
-           "ccnn_debug_stage1_map", "ccnn_debug_candidates")
+           "ccnn_debug_stage1_map", "ccnn_debug_candidates", "ccnn_debug_counters")
 
 
 class CcnnError(RuntimeError):
@@ -100,6 +102,7 @@ def load():
     L.ccnn_debug_level.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_uint8), C.c_int64]
     L.ccnn_debug_stage1_map.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_float), C.c_int64]
     L.ccnn_debug_candidates.argtypes = [C.c_void_p, _P(Candidate), C.c_int64, _P(C.c_int64)]
+    L.ccnn_debug_counters.argtypes = [C.c_void_p, _P(C.c_uint32), C.c_int]
     _lib = L
     return L
 
@@ -217,6 +220,11 @@ class Detector:
         self._check(load().ccnn_debug_stage1_map(self.h, frame, level,
                                                  out.ctypes.data_as(_P(C.c_float)), out.size))
         return out
+
+    def counters(self):
+        out = (C.c_uint32 * 16)()
+        n = load().ccnn_debug_counters(self.h, out, 16)
+        return list(out[:max(n, 0)])
 
     def candidates(self):
         L = load()

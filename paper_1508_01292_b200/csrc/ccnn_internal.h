@@ -18,7 +18,9 @@ constexpr int kPatchN = kPatchW * kPatchH;      // 2805
 constexpr int kResp = 25;                       // 5x5 response map
 
 // ---- weights, laid out for compile-time indexing (kernel parameters = constant bank) ----
-struct Cnn1W {                 // 797 floats
+struct __align__(16) Cnn1W {   // 797 weights + re-arranged copies for the stage-1 kernel
+    float w2v[6][56];          // layer 2 per input map ci: [o*9 + ky*3 + kx] (54 used), float4 blocks
+    float w3v[6][60];          // layer 3 per input map ci: [i][m][kx], i = 5 - ky (streaming order)
     float w1[6][16], b1[6];    // [out][ky*4+kx]
     float w2[6][6][9], b2[6];  // [out][in][ky*3+kx]
     float w3[2][6][30], b3[2]; // [out][in][ky*5+kx]
@@ -88,12 +90,15 @@ void launch_pyramid(const uint8_t* frames, int64_t frame_stride, int64_t pitch, 
                     uint8_t* levels, int64_t level_frame_stride, const LevelInfo* d_levels,
                     const LevelInfo* h_levels, int n_levels, const uint32_t* d_tabs, int n,
                     cudaStream_t s);
-// stage 1 (fused CNN1 + threshold + compaction), persistent over the task table
+// stage 1 (fused CNN1 + threshold + compaction): a persistent grid of stage1_grid() CTAs,
+// CTA b runs tasks[cta_first[b] .. cta_first[b+1]) (host LPT schedule)
 void launch_stage1(const Cnn1W& w, float T1, const uint8_t* levels, int64_t level_frame_stride,
-                   const LevelInfo* d_levels, const S1Task* d_tasks, int n_tasks, S1Cand* cands,
-                   uint32_t cand_cap, Ctrl* ctrl, float* dbg_map, int64_t dbg_map_frame_stride,
-                   int sm_count, cudaStream_t s);
-int stage1_band_width();       // TW of the compiled stage-1 kernel
+                   const LevelInfo* d_levels, const S1Task* d_tasks, const int32_t* d_cta_first,
+                   int grid, S1Cand* cands, uint32_t cand_cap, Ctrl* ctrl, float* dbg_map,
+                   int64_t dbg_map_frame_stride, cudaStream_t s);
+int stage1_band_width();          // TW of the compiled stage-1 kernel
+int stage1_grid(int sm_count);    // CTAs of the persistent stage-1 launch
+int stage1_task_cost(int nrows);  // relative cost of a task (super-steps)
 // selective unit (stage 2/3), persistent over the survivor queue
 struct SelParams { float T2a, T2b; int32_t Tnn, rule; };
 void launch_selective(const Cnn2W& w2, const Cnn3W& w3, SelParams sp, const uint8_t* frames,

@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <functional>
+#include <queue>
 
 #include "../../include/ccnn.h"
 #include "ccnn_internal.h"
@@ -69,18 +71,20 @@ struct ccnn_ctx {
     int min_cluster = 1;
     int max_w = 0, max_h = 0, max_batch = 0;
     int queue_cap = 4096;
-    int seg_rows = 64;
+    int seg_rows_param = 0;             // 0 = adaptive
 
     // plan (cached per batch shape)
     PlanKey key;
     std::vector<LevelInfo> levels;
-    std::vector<S1Task> tasks;
+    std::vector<S1Task> tasks;          // grouped by CTA (LPT schedule)
+    std::vector<int32_t> cta_first;     // stage1_grid + 1 offsets into tasks
+    int s1_grid = 0;
     std::vector<uint32_t> tabs;
     int64_t level_frame_stride = 0;
     int64_t map_frame_stride = 0;
     int64_t windows_per_frame = 0;
 
-    DevBuf frames, arena, d_levels, d_tasks, d_tabs, cands, selout, dbg_resp, acc, ctrl, staging,
+    DevBuf frames, arena, d_levels, d_tasks, d_cta_first, d_tabs, cands, selout, dbg_resp, acc, ctrl, staging,
         counts, out, dbg_map;
     Ctrl* h_ctrl = nullptr;                 // pinned readback
     cudaEvent_t ev[6] = {};
@@ -147,6 +151,12 @@ void unpack_cnn1(const float* w, Cnn1W& o)
     std::memcpy(o.b3, p, sizeof(o.b3)); p += 2;
     std::memcpy(o.w4, p, sizeof(o.w4)); p += 2;
     o.b4 = *p;
+    for (int ci = 0; ci < 6; ++ci) {                 // vector-friendly copies (stage1.cu)
+        for (int k = 0; k < 56; ++k) o.w2v[ci][k] = k < 54 ? o.w2[k / 9][ci][k % 9] : 0.f;
+        for (int i = 0; i < 6; ++i)
+            for (int m = 0; m < 2; ++m)
+                for (int kx = 0; kx < 5; ++kx) o.w3v[ci][(i * 2 + m) * 5 + kx] = o.w3[m][ci][(5 - i) * 5 + kx];
+    }
 }
 template <int A, int B, int C>
 void unpack_sel(const float* p, SelNetW<A, B, C>& o)
@@ -214,32 +224,60 @@ void build_plan(ccnn_ctx* c, int n, int W, int H, int min_face, float scale_step
     c->level_frame_stride = round_up(off + 256, 256);
     c->map_frame_stride = map_off;
     const int TW = stage1_band_width();
+    // segment height: the tallest segments (least vertical halo recompute) whose largest
+    // task still fits in half the average load of a CTA slot, so the dynamic list schedule
+    // balances (ccnn_params.segment_rows > 0 forces a height)
+    auto make_tasks = [&](int seg, std::vector<S1Task>& one) {
+        one.clear();
+        for (int l = 0; l < (int)c->levels.size(); ++l) {
+            const LevelInfo& L = c->levels[l];
+            const int nseg = std::max(1, (L.ny + seg - 1) / seg);
+            const int rows = (L.ny + nseg - 1) / nseg;
+            for (int x0 = 0; x0 < L.nx; x0 += TW)
+                for (int y0 = 0; y0 < L.ny; y0 += rows) {
+                    S1Task t{};
+                    t.level = (int16_t)l;
+                    t.bw = (int16_t)std::min(TW, L.nx - x0);
+                    t.x0 = (int16_t)x0;
+                    t.y0 = (int16_t)y0;
+                    t.nrows = (int16_t)std::min(rows, L.ny - y0);
+                    one.push_back(t);
+                }
+        }
+    };
     std::vector<S1Task> one;
-    for (int l = 0; l < (int)c->levels.size(); ++l) {
-        const LevelInfo& L = c->levels[l];
-        const int nseg = std::max(1, (L.ny + c->seg_rows - 1) / c->seg_rows);
-        const int rows = (L.ny + nseg - 1) / nseg;
-        for (int x0 = 0; x0 < L.nx; x0 += TW)
-            for (int y0 = 0; y0 < L.ny; y0 += rows) {
-                S1Task t{};
-                t.level = (int16_t)l;
-                t.bw = (int16_t)std::min(TW, L.nx - x0);
-                t.x0 = (int16_t)x0;
-                t.y0 = (int16_t)y0;
-                t.nrows = (int16_t)std::min(rows, L.ny - y0);
-                one.push_back(t);
+    if (c->seg_rows_param > 0) {
+        make_tasks(c->seg_rows_param, one);
+    } else {
+        for (int seg : {1 << 14, 256, 192, 128, 96, 64, 48, 32, 24, 16}) {
+            make_tasks(seg, one);
+            int64_t total = 0, biggest = 0;
+            for (const S1Task& t : one) {
+                total += stage1_task_cost(t.nrows);
+                biggest = std::max<int64_t>(biggest, stage1_task_cost(t.nrows));
             }
+            total *= n;
+            if (2 * biggest * c->s1_grid <= total) break;
+        }
     }
-    // longest tasks first (cost ~ nrows + 8 steps regardless of band width), frames interleaved
-    std::stable_sort(one.begin(), one.end(),
-                     [](const S1Task& a, const S1Task& b) { return a.nrows > b.nrows; });
-    c->tasks.reserve(one.size() * n);
-    for (const S1Task& t : one)
-        for (int f = 0; f < n; ++f) {
+    // LPT schedule: tasks of all frames, longest first, each to the least-loaded CTA of
+    // the persistent grid (cost ~ super-steps, independent of the band width)
+    std::vector<S1Task> all;
+    all.reserve(one.size() * n);
+    for (int f = 0; f < n; ++f)
+        for (const S1Task& t : one) {
             S1Task u = t;
             u.frame = f;
-            c->tasks.push_back(u);
+            all.push_back(u);
         }
+    std::stable_sort(all.begin(), all.end(),
+                     [](const S1Task& a, const S1Task& b) { return a.nrows > b.nrows; });
+    // the kernel takes tasks in this order from an atomic counter (greedy list scheduling);
+    // cta_first = {0, ..., 0, n_tasks}: grid size + total task count for the launch
+    const int G = std::max(1, std::min<int>(c->s1_grid, (int)all.size()));
+    c->tasks = all;
+    c->cta_first.assign(G + 1, 0);
+    c->cta_first[G] = (int32_t)all.size();
 }
 
 }  // namespace
@@ -291,7 +329,9 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
     ctx->max_h = p->max_h;
     ctx->max_batch = p->max_batch;
     ctx->queue_cap = p->queue_capacity > 0 ? p->queue_capacity : 4096;
-    ctx->seg_rows = p->segment_rows > 0 ? p->segment_rows : 64;
+    ctx->seg_rows_param = p->segment_rows;
+    ctx->s1_grid = stage1_grid(ctx->sm_count);
+    CU(cudaGetLastError());
     CU(cudaMallocHost(&ctx->h_ctrl, sizeof(Ctrl)));
     for (auto& e : ctx->ev) CU(cudaEventCreate(&e));
     CU(ctx->ctrl.ensure(sizeof(Ctrl)));
@@ -318,7 +358,7 @@ void ccnn_destroy(ccnn_ctx* ctx)
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream); else cudaDeviceSynchronize();
-    for (DevBuf* b : {&ctx->frames, &ctx->arena, &ctx->d_levels, &ctx->d_tasks, &ctx->d_tabs,
+    for (DevBuf* b : {&ctx->frames, &ctx->arena, &ctx->d_levels, &ctx->d_tasks, &ctx->d_cta_first, &ctx->d_tabs,
                       &ctx->cands, &ctx->selout, &ctx->dbg_resp, &ctx->acc, &ctx->ctrl,
                       &ctx->staging, &ctx->counts, &ctx->out, &ctx->dbg_map})
         b->release();
@@ -371,6 +411,7 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
     CU(ctx->arena.ensure((size_t)ctx->level_frame_stride * n));
     CU(ctx->d_levels.ensure(sizeof(LevelInfo) * L));
     CU(ctx->d_tasks.ensure(sizeof(S1Task) * ctx->tasks.size()));
+    CU(ctx->d_cta_first.ensure(sizeof(int32_t) * ctx->cta_first.size()));
     CU(ctx->d_tabs.ensure(sizeof(uint32_t) * ctx->tabs.size()));
     CU(ctx->cands.ensure(sizeof(S1Cand) * cand_cap));
     CU(ctx->selout.ensure(sizeof(SelOut) * cand_cap));
@@ -390,6 +431,8 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
                            cudaMemcpyHostToDevice, s));
         CU(cudaMemcpyAsync(ctx->d_tabs.p, ctx->tabs.data(), sizeof(uint32_t) * ctx->tabs.size(),
                            cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(ctx->d_cta_first.p, ctx->cta_first.data(),
+                           sizeof(int32_t) * ctx->cta_first.size(), cudaMemcpyHostToDevice, s));
         CU(cudaStreamSynchronize(s));   // host vectors may change on the next replan
     }
     ctx->key = key;
@@ -412,9 +455,10 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
                    ctx->d_levels.as<LevelInfo>(), ctx->levels.data(), L, ctx->d_tabs.as<uint32_t>(), n, s);
     if (timing) CU(cudaEventRecord(ctx->ev[2], s));
     launch_stage1(ctx->w1, ctx->T1, ctx->arena.as<uint8_t>(), ctx->level_frame_stride,
-                  ctx->d_levels.as<LevelInfo>(), ctx->d_tasks.as<S1Task>(), (int)ctx->tasks.size(),
+                  ctx->d_levels.as<LevelInfo>(), ctx->d_tasks.as<S1Task>(),
+                  ctx->d_cta_first.as<int32_t>(), (int)ctx->cta_first.size() - 1,
                   ctx->cands.as<S1Cand>(), cand_cap, ctx->ctrl.as<Ctrl>(),
-                  dbg1 ? ctx->dbg_map.as<float>() : nullptr, ctx->map_frame_stride, ctx->sm_count, s);
+                  dbg1 ? ctx->dbg_map.as<float>() : nullptr, ctx->map_frame_stride, s);
     if (timing) CU(cudaEventRecord(ctx->ev[3], s));
     launch_selective(ctx->w2, ctx->w3, ctx->sp, dframes, fstride, dpitch, w, h,
                      ctx->d_levels.as<LevelInfo>(), ctx->cands.as<S1Cand>(), cand_cap,
@@ -502,14 +546,22 @@ int ccnn_debug_stage1_map(ccnn_ctx* ctx, int frame, int level, float* out, int64
     return CCNN_OK;
 }
 
+int ccnn_debug_counters(ccnn_ctx* ctx, uint32_t* out, int cap)
+{
+    if (!ctx || !out) return CCNN_E_ARG;
+    const int n = (int)(sizeof(ctx->h_ctrl->pad) / sizeof(uint32_t));
+    for (int k = 0; k < n && k < cap; ++k) out[k] = ctx->h_ctrl->pad[k];
+    return n;
+}
+
 int ccnn_debug_candidates(ccnn_ctx* ctx, ccnn_candidate* out, int64_t cap, int64_t* n)
 {
     if (!ctx || !n) return CCNN_E_ARG;
     if (!ctx->last_valid) return fail(ctx, CCNN_E_STATE, "no completed detect");
     const int64_t cnt = ctx->last_cands;
     *n = cnt;
-    if (cnt == 0) return CCNN_OK;
-    if (!out || cap < cnt) return fail(ctx, CCNN_E_CAPACITY, "cap < candidate count");
+    if (cnt == 0 || !out) return CCNN_OK;            // count query
+    if (cap < cnt) return fail(ctx, CCNN_E_CAPACITY, "cap < candidate count");
     CU(cudaSetDevice(ctx->device));
     std::vector<S1Cand> c(cnt);
     std::vector<SelOut> so(cnt);

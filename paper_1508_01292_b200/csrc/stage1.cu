@@ -9,18 +9,24 @@
 // Eq. 1 activation after every conv, fp32.
 //
 // B200 design (not the paper's Kepler texture kernels):
-//  * one persistent kernel over a flattened (frame, level, band, row-segment) task table,
-//    longest tasks first, dynamic atomic task counter -> no per-level launches;
-//  * a CTA owns a band of TW = NT/2-5 windows and marches down its rows with a
-//    line-buffer pipeline in shared memory: input ring (fp32, even/odd de-interleaved
-//    columns so every LDS is bank-conflict free), pooled-layer-1 ring, pooled-layer-2
-//    ring; only ONE __syncthreads per window row, each phase reads rows written in
-//    earlier steps; no vertical halo recompute inside a task;
-//  * every MAC is an FFMA whose weight operand is a constant-bank kernel parameter
-//    (fully unrolled, compile-time indices) -> two register operands per FFMA;
-//  * max-pool BEFORE the activation (Eq. 1 is monotone: act(max) == max(act), 4x fewer
-//    activations); layer 3 streams its 6 kernel rows through register accumulators;
+//  * one persistent launch per batch; a CTA owns a band of TW = 59 windows of one level
+//    (128 pooled-layer-1 columns, 63 pooled-layer-2 columns) and a segment of its rows;
+//    the host assigns (frame, level, band, segment) tasks to CTAs longest-first (LPT),
+//    so no per-level launches (the paper's small-level launch overhead);
+//  * line-buffer pipeline in shared memory marching down the band, TWO window rows per
+//    "super-step", two __syncthreads per super-step (layer 1 | loader + layers 2, 3):
+//    input ring (fp32, even/odd de-interleaved columns -> conflict-free LDS), pooled-
+//    layer-1 ring, pooled-layer-2 ring, 40 KB in all -> 5 CTAs per SM;
+//  * work is split over DATA only (columns x rows), never over maps or taps, so all 128
+//    threads run one instruction stream whose weights are warp-uniform: every MAC is an
+//    FFMA with a uniform-register (constant-bank kernel parameter) operand, rolled loops
+//    index the constant bank with uniform counters (LDCU [UR+imm]);
+//  * max-pool BEFORE the activation (Eq. 1 is monotone: act(max) == max(act));
+//    layer 3 streams P2 rows through register accumulators, the even/odd rows of a pair
+//    on adjacent lanes, partial sums combined with one shfl per output;
 //  * threshold + warp ballot/popc + ONE atomicAdd per warp into the survivor queue.
+#include <algorithm>
+
 #include "ccnn_internal.h"
 
 namespace ccnn {
@@ -38,71 +44,77 @@ __device__ __forceinline__ float act(float x)
     return copysignf(fmaf(-1.7159f, r, 1.7159f), x);
 }
 
-template <int NT>
-struct Cfg {
-    static constexpr int TW = NT / 2 - 5;        // windows per band
-    static constexpr int P2C = NT / 2 - 1;       // pooled layer-2 columns = TW + 4
-    static constexpr int IN_WORDS = NT / 2 + 1;  // 32-bit words per input row (>= 2NT+3 B)
-    static constexpr int IN_ODD = NT + 4;        // odd columns start inside an input row
-    static constexpr int IN_RS = 2 * NT + 8;     // input ring row stride (floats)
-    static constexpr int IN_RING = 12;
-    static constexpr int P1_ODD = NT / 2 + 16;   // odd P1 columns start (bank offset 16)
-    static constexpr int P1_RS = NT + 16;        // one (row, map) of the P1 ring
-    static constexpr int P1_RING = 6;
-    static constexpr int P2_RS = NT / 2 + 8;
-    static constexpr int P2_RING = 2;
-    static constexpr int SMEM_FLOATS = IN_RING * IN_RS + P1_RING * 6 * P1_RS + P2_RING * 6 * P2_RS;
-    static constexpr int LOAD_SLOTS = (4 * IN_WORDS + NT - 1) / NT;
-};
+#ifndef S1_MIN_BLOCKS
+#define S1_MIN_BLOCKS 5
+#endif
+
+constexpr int NT = 128;                 // threads per CTA
+constexpr int TW = NT / 2 - 5;          // 59 windows per band
+constexpr int IN_WORDS = NT / 2 + 1;    // 65 32-bit words cover the 4*TW+23 = 259 input columns
+constexpr int IN_ODD = NT + 4;          // odd input columns start inside a ring row
+constexpr int IN_RS = 2 * NT + 8;       // input ring row stride (floats)
+constexpr int IN_RING = 12;             // rows 8v .. 8v+10 (+ 8v+11 .. 8v+18 after the mid barrier)
+constexpr int P1_ODD = NT / 2 + 16;     // odd P1 columns start (bank offset 16)
+constexpr int P1_RS = NT + 16;          // one (row, map) of the P1 ring
+constexpr int P1_RING = 6;              // rows 4v-2 .. 4v+3
+constexpr int P2_RS = NT / 2 + 8;
+constexpr int P2_RING = 4;              // rows 2v-3 .. 2v
+constexpr int SMEM_FLOATS = IN_RING * IN_RS + P1_RING * 6 * P1_RS + P2_RING * 6 * P2_RS;
+constexpr int LOAD_WORDS = 8 * IN_WORDS;                 // 8 new input rows per super-step
+constexpr int LOAD_SLOTS = (LOAD_WORDS + NT - 1) / NT;
 
 __device__ __forceinline__ float u8f(uint32_t v)
 {
     return fmaf((float)v, 1.0f / 127.5f, -1.0f);   // O3: (v - 127.5) / 127.5
 }
 
-template <int NT>
 __device__ __forceinline__ void store_word(float* ring, int slot, int w, uint32_t word)
 {
-    using C = Cfg<NT>;
-    float* row = ring + slot * C::IN_RS;
-    float2 ev = make_float2(u8f(word & 0xFFu), u8f((word >> 16) & 0xFFu));
-    float2 od = make_float2(u8f((word >> 8) & 0xFFu), u8f(word >> 24));
+    float* row = ring + slot * IN_RS;
+    const float2 ev = make_float2(u8f(word & 0xFFu), u8f((word >> 16) & 0xFFu));
+    const float2 od = make_float2(u8f((word >> 8) & 0xFFu), u8f(word >> 24));
     *reinterpret_cast<float2*>(row + 2 * w) = ev;
-    *reinterpret_cast<float2*>(row + C::IN_ODD + 2 * w) = od;
+    *reinterpret_cast<float2*>(row + IN_ODD + 2 * w) = od;
 }
 
-template <int NT, bool DEBUG>
-__global__ void __launch_bounds__(NT, 512 / NT) stage1_kernel(
+__device__ __forceinline__ int pmod(int a, int m) { return ((a % m) + m) % m; }
+
+template <bool DEBUG>
+__global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
     const __grid_constant__ Cnn1W W, const float T1,
     const uint8_t* __restrict__ levels, const int64_t level_frame_stride,
-    const LevelInfo* __restrict__ lvinfo, const S1Task* __restrict__ tasks, const int n_tasks,
-    S1Cand* __restrict__ cands, const uint32_t cand_cap, Ctrl* __restrict__ ctrl,
-    float* __restrict__ dbg_map, const int64_t dbg_map_frame_stride)
+    const LevelInfo* __restrict__ lvinfo, const S1Task* __restrict__ tasks,
+    const int32_t* __restrict__ cta_first, S1Cand* __restrict__ cands, const uint32_t cand_cap,
+    Ctrl* __restrict__ ctrl, float* __restrict__ dbg_map, const int64_t dbg_map_frame_stride)
 {
-    using C = Cfg<NT>;
     extern __shared__ __align__(16) float smem[];
     float* const in_ring = smem;
-    float* const p1_ring = in_ring + C::IN_RING * C::IN_RS;
-    float* const p2_ring = p1_ring + C::P1_RING * 6 * C::P1_RS;
-    __shared__ int s_task;
+    float* const p1_ring = in_ring + IN_RING * IN_RS;
+    float* const p2_ring = p1_ring + P1_RING * 6 * P1_RS;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int half = tid / (NT / 2);           // 0: L2 maps 0-1 + L3; 1: L2 maps 2-5
-    const int q = tid & (NT / 2 - 1);          // P2 column (L2) / window column (L3)
+    const int warp = tid >> 5;
+    // layer-2 thread -> (P2 column q2, row r2 of the super-step's pair)
+    const int q2 = 32 * (warp & 1) + lane;
+    const int r2 = warp >> 1;
+    // layer-3 thread -> (window column j3, P2 row parity r3); pairs on adjacent lanes
+    const int j3 = 16 * warp + (lane >> 1);
+    const int r3 = lane & 1;
 
-    // loader slots: word k -> (row k / IN_WORDS, word k % IN_WORDS) of a 4-row group
-    int ld_row[C::LOAD_SLOTS], ld_w[C::LOAD_SLOTS];
-    bool ld_ok[C::LOAD_SLOTS];
+    int ld_row[LOAD_SLOTS], ld_w[LOAD_SLOTS];
+    bool ld_ok[LOAD_SLOTS];
 #pragma unroll
-    for (int k = 0; k < C::LOAD_SLOTS; ++k) {
+    for (int k = 0; k < LOAD_SLOTS; ++k) {
         const int g = tid + k * NT;
-        ld_ok[k] = g < 4 * C::IN_WORDS;
-        ld_row[k] = g / C::IN_WORDS;
-        ld_w[k] = g % C::IN_WORDS;
+        ld_ok[k] = g < LOAD_WORDS;
+        ld_row[k] = g / IN_WORDS;
+        ld_w[k] = g % IN_WORDS;
     }
 
-    for (;;) {
+    __shared__ int s_task;
+    const int n_tasks = cta_first[gridDim.x];
+    for (;;) {                                   // dynamic list scheduling, longest tasks first
         if (tid == 0) s_task = (int)atomicAdd(&ctrl->task_next, 1u);
         __syncthreads();
         const int ti = s_task;
@@ -112,236 +124,252 @@ __global__ void __launch_bounds__(NT, 512 / NT) stage1_kernel(
         const int nrows = T.nrows;
         const uint8_t* const band = levels + (int64_t)T.frame * level_frame_stride + L.offset +
                                     (int64_t)(4 * T.x0);
-        const int row_base = 4 * T.y0;                 // first level row of the task
-        const int wmax = (L.pitch - 4 * T.x0) / 4 - 1; // last readable word in a row
+        const int row_base = 4 * T.y0;
+        const int wmax = (L.pitch - 4 * T.x0) / 4 - 1;
         auto gword = [&](int r, int w) -> uint32_t {
             const int lr = min(row_base + r, L.lh - 1);
             const int ww = min(w, wmax);
             return __ldg(reinterpret_cast<const uint32_t*>(band + (int64_t)lr * L.pitch) + ww);
         };
 
-        // prologue: rows 0..6 straight to the ring, rows 7..10 into registers
-        for (int g = tid; g < 7 * C::IN_WORDS; g += NT)
-            store_word<NT>(in_ring, g / C::IN_WORDS, g % C::IN_WORDS,
-                           gword(g / C::IN_WORDS, g % C::IN_WORDS));
-        uint32_t pre[C::LOAD_SLOTS];
+        // prologue: input rows 0..10 to the ring, rows 11..18 into registers
+        for (int g = tid; g < 11 * IN_WORDS; g += NT)
+            store_word(in_ring, g / IN_WORDS, g % IN_WORDS, gword(g / IN_WORDS, g % IN_WORDS));
+        uint32_t pre[LOAD_SLOTS];
 #pragma unroll
-        for (int k = 0; k < C::LOAD_SLOTS; ++k)
-            pre[k] = ld_ok[k] ? gword(7 + ld_row[k], ld_w[k]) : 0u;
+        for (int k = 0; k < LOAD_SLOTS; ++k) pre[k] = ld_ok[k] ? gword(11 + ld_row[k], ld_w[k]) : 0u;
 
-        float acc3[2][6];
+        float acc3[2][6], carry[2] = {0.f, 0.f};
 #pragma unroll
         for (int m = 0; m < 2; ++m)
 #pragma unroll
             for (int i = 0; i < 6; ++i) acc3[m][i] = 0.f;
         __syncthreads();
 
-        const int nsteps = nrows + 8;
-        for (int s = 0; s < nsteps; ++s) {
-            // ---- loader: commit rows 4s+7..4s+10, prefetch rows 4s+11..4s+14 ----
-#pragma unroll
-            for (int k = 0; k < C::LOAD_SLOTS; ++k)
-                if (ld_ok[k]) store_word<NT>(in_ring, (4 * s + 7 + ld_row[k]) % C::IN_RING, ld_w[k], pre[k]);
-#pragma unroll
-            for (int k = 0; k < C::LOAD_SLOTS; ++k)
-                pre[k] = ld_ok[k] ? gword(4 * s + 11 + ld_row[k], ld_w[k]) : 0u;
-
-            // ---- L1: conv4x4 1->6 + pool + act -> P1 rows 2s, 2s+1 (input rows 4s..4s+6) ----
-            if (s <= nrows + 5) {
-                const int c = tid;                    // P1 column
+        const int nsteps = (nrows + 7) / 2 + 1;      // ceil((nrows + 6) / 2) + 1
+        for (int v = 0; v < nsteps; ++v) {
+            // ---- L1: conv4x4 1->6, pool, act -> P1 rows 4v .. 4v+3 (input rows 8v .. 8v+10);
+            //      thread = P1 column, two row pairs ----
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int c = tid;
                 float x[7][5];
-                const int s4 = (4 * s) % C::IN_RING;
+                const int r0 = (8 * v + 4 * h) % IN_RING;
 #pragma unroll
                 for (int rr = 0; rr < 7; ++rr) {
-                    int slot = s4 + rr;
-                    slot = slot >= C::IN_RING ? slot - C::IN_RING : slot;
-                    const float* row = in_ring + slot * C::IN_RS;
+                    int slot = r0 + rr;
+                    slot = slot >= IN_RING ? slot - IN_RING : slot;
+                    const float* row = in_ring + slot * IN_RS;
                     x[rr][0] = row[c];
-                    x[rr][1] = row[C::IN_ODD + c];
+                    x[rr][1] = row[IN_ODD + c];
                     x[rr][2] = row[c + 1];
-                    x[rr][3] = row[C::IN_ODD + c + 1];
+                    x[rr][3] = row[IN_ODD + c + 1];
                     x[rr][4] = row[c + 2];
                 }
-                const int pcol = (c & 1) ? C::P1_ODD + (c >> 1) : (c >> 1);
+                const int pcol = (c & 1) ? P1_ODD + (c >> 1) : (c >> 1);
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
-                    float mx[6];
+                    float a[4][6];                    // the 2x2 conv outputs of one pool cell
 #pragma unroll
-                    for (int o = 0; o < 6; ++o) mx[o] = -INFINITY;
+                    for (int p = 0; p < 4; ++p) {
+                        const int py = p >> 1, px = p & 1;
 #pragma unroll
-                    for (int py = 0; py < 2; ++py)
+                        for (int o = 0; o < 6; ++o) a[p][o] = W.b1[o];
 #pragma unroll
-                        for (int px = 0; px < 2; ++px) {
-                            float a[6];
+                        for (int ky = 0; ky < 4; ++ky)
 #pragma unroll
-                            for (int o = 0; o < 6; ++o) a[o] = W.b1[o];
+                            for (int kx = 0; kx < 4; ++kx) {
+                                const float xv = x[2 * r + py + ky][px + kx];
 #pragma unroll
-                            for (int ky = 0; ky < 4; ++ky)
-#pragma unroll
-                                for (int kx = 0; kx < 4; ++kx) {
-                                    const float v = x[2 * r + py + ky][px + kx];
-#pragma unroll
-                                    for (int o = 0; o < 6; ++o) a[o] = fmaf(W.w1[o][ky * 4 + kx], v, a[o]);
-                                }
-#pragma unroll
-                            for (int o = 0; o < 6; ++o) mx[o] = fmaxf(mx[o], a[o]);
-                        }
-                    const int slot = (2 * s + r) % C::P1_RING;
+                                for (int o = 0; o < 6; ++o) a[p][o] = fmaf(W.w1[o][ky * 4 + kx], xv, a[p][o]);
+                            }
+                    }
+                    const int slot = (4 * v + 2 * h + r) % P1_RING;
 #pragma unroll
                     for (int o = 0; o < 6; ++o)
-                        p1_ring[(slot * 6 + o) * C::P1_RS + pcol] = act(mx[o]);
+                        p1_ring[(slot * 6 + o) * P1_RS + pcol] =
+                            act(fmaxf(fmaxf(a[0][o], a[1][o]), fmaxf(a[2][o], a[3][o])));
                 }
             }
 
-            // ---- L2: conv3x3 6->6 + pool + act -> P2 row s-2 (P1 rows 2s-4..2s-1) ----
-            if (s >= 2 && s <= nrows + 6) {
-                const int pslot = (s - 2) & 1;
+            __syncthreads();   // P1 rows 4v..4v+3 visible; input rows 8v..8v+7 dead
+
+            // ---- loader: input rows 8v+11 .. 8v+18 into the slots of 8v .. 8v+7 (fetched
+            //      during the previous super-step), then prefetch rows 8v+19 .. 8v+26 ----
+#pragma unroll
+            for (int k = 0; k < LOAD_SLOTS; ++k)
+                if (ld_ok[k]) store_word(in_ring, (8 * v + 11 + ld_row[k]) % IN_RING, ld_w[k], pre[k]);
+#pragma unroll
+            for (int k = 0; k < LOAD_SLOTS; ++k)
+                pre[k] = ld_ok[k] ? gword(8 * v + 19 + ld_row[k], ld_w[k]) : 0u;
+
+            // ---- L2: conv3x3 6->6, pool, act -> P2 row p = 2v-1+r2 (P1 rows 2p .. 2p+3) ----
+            {
+                const int p = 2 * v - 1 + r2;
                 int rs[4];
 #pragma unroll
-                for (int rr = 0; rr < 4; ++rr) rs[rr] = (2 * s - 4 + rr) % C::P1_RING;
-                auto l2 = [&](auto M0c, auto NMc) {
-                    constexpr int M0 = decltype(M0c)::value, NM = decltype(NMc)::value;
-                    float a[NM][4];
+                for (int rr = 0; rr < 4; ++rr) rs[rr] = pmod(2 * p + rr, P1_RING);
+                float a[6][4];
 #pragma unroll
-                    for (int o = 0; o < NM; ++o)
+                for (int o = 0; o < 6; ++o)
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) a[o][k] = W.b2[M0 + o];
+                    for (int k = 0; k < 4; ++k) a[o][k] = W.b2[o];
+#pragma unroll 1
+                for (int ci = 0; ci < 6; ++ci) {
+                    float xv[4][4];
 #pragma unroll
-                    for (int ci = 0; ci < 6; ++ci) {
-                        float v[4][4];
+                    for (int rr = 0; rr < 4; ++rr) {
+                        const float* row = p1_ring + (rs[rr] * 6 + ci) * P1_RS;
+                        xv[rr][0] = row[q2];
+                        xv[rr][1] = row[P1_ODD + q2];
+                        xv[rr][2] = row[q2 + 1];
+                        xv[rr][3] = row[P1_ODD + q2 + 1];
+                    }
+                    // explicit 16-byte loads of the parameter block -> LDCU [UR+imm]
+                    float wv[56];
+                    const float4* w4p = reinterpret_cast<const float4*>(W.w2v[ci]);
 #pragma unroll
-                        for (int rr = 0; rr < 4; ++rr) {
-                            const float* row = p1_ring + (rs[rr] * 6 + ci) * C::P1_RS;
-                            v[rr][0] = row[q];
-                            v[rr][1] = row[C::P1_ODD + q];
-                            v[rr][2] = row[q + 1];
-                            v[rr][3] = row[C::P1_ODD + q + 1];
-                        }
-#pragma unroll
-                        for (int o = 0; o < NM; ++o)
-#pragma unroll
-                            for (int py = 0; py < 2; ++py)
-#pragma unroll
-                                for (int px = 0; px < 2; ++px)
-#pragma unroll
-                                    for (int ky = 0; ky < 3; ++ky)
-#pragma unroll
-                                        for (int kx = 0; kx < 3; ++kx)
-                                            a[o][py * 2 + px] = fmaf(W.w2[M0 + o][ci][ky * 3 + kx],
-                                                                     v[py + ky][px + kx], a[o][py * 2 + px]);
+                    for (int k4 = 0; k4 < 14; ++k4) {
+                        const float4 t4 = w4p[k4];
+                        wv[4 * k4] = t4.x; wv[4 * k4 + 1] = t4.y; wv[4 * k4 + 2] = t4.z; wv[4 * k4 + 3] = t4.w;
                     }
 #pragma unroll
-                    for (int o = 0; o < NM; ++o) {
-                        const float m = fmaxf(fmaxf(a[o][0], a[o][1]), fmaxf(a[o][2], a[o][3]));
-                        p2_ring[(pslot * 6 + M0 + o) * C::P2_RS + q] = act(m);
-                    }
-                };
-                if (half == 0) l2(std::integral_constant<int, 0>{}, std::integral_constant<int, 2>{});
-                else           l2(std::integral_constant<int, 2>{}, std::integral_constant<int, 4>{});
+                    for (int o = 0; o < 6; ++o)
+#pragma unroll
+                        for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+                            for (int kx = 0; kx < 3; ++kx) {
+                                const float w = wv[o * 9 + ky * 3 + kx];
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    a[o][k] = fmaf(w, xv[(k >> 1) + ky][(k & 1) + kx], a[o][k]);
+                            }
+                }
+                const int pslot = pmod(p, P2_RING);
+#pragma unroll
+                for (int o = 0; o < 6; ++o)
+                    p2_ring[(pslot * 6 + o) * P2_RS + q2] =
+                        act(fmaxf(fmaxf(a[o][0], a[o][1]), fmaxf(a[o][2], a[o][3])));
             }
 
-            // ---- L3 (+L4): conv5x6 6->2 streamed over P2 row s-3; C1x1 2->1; threshold ----
-            if (half == 0 && s >= 3) {
-                const int j = q;                       // window column in the band
-                const float* p2 = p2_ring + ((s - 3) & 1) * 6 * C::P2_RS;
-#pragma unroll
+            // ---- L3: conv5x6 6->2 streamed over P2 row p = 2v-3+r3 (written in the previous
+            //      super-step) -> outputs p-5 .. p ----
+            {
+                const int p = 2 * v - 3 + r3;
+                const float* p2 = p2_ring + pmod(p, P2_RING) * 6 * P2_RS;
+#pragma unroll 1
                 for (int ci = 0; ci < 6; ++ci) {
-                    float v[5];
+                    float xv[5];
 #pragma unroll
-                    for (int kx = 0; kx < 5; ++kx) v[kx] = p2[ci * C::P2_RS + j + kx];
+                    for (int kx = 0; kx < 5; ++kx) xv[kx] = p2[ci * P2_RS + j3 + kx];
+                    float wv[60];
+                    const float4* w4p = reinterpret_cast<const float4*>(W.w3v[ci]);
+#pragma unroll
+                    for (int k4 = 0; k4 < 15; ++k4) {
+                        const float4 t4 = w4p[k4];
+                        wv[4 * k4] = t4.x; wv[4 * k4 + 1] = t4.y; wv[4 * k4 + 2] = t4.z; wv[4 * k4 + 3] = t4.w;
+                    }
 #pragma unroll
                     for (int i = 0; i < 6; ++i)
 #pragma unroll
                         for (int m = 0; m < 2; ++m)
 #pragma unroll
                             for (int kx = 0; kx < 5; ++kx)
-                                acc3[m][i] = fmaf(W.w3[m][ci][(5 - i) * 5 + kx], v[kx], acc3[m][i]);
+                                acc3[m][i] = fmaf(wv[(i * 2 + m) * 5 + kx], xv[kx], acc3[m][i]);
                 }
-                const int o = s - 8;                   // finished window row (task-relative)
-                if (o >= 0) {
-                    const float a0 = act(acc3[0][0] + W.b3[0]);
-                    const float a1 = act(acc3[1][0] + W.b3[1]);
-                    const float score = act(fmaf(W.w4[1], a1, fmaf(W.w4[0], a0, W.b4)));
-                    const bool valid = (j < T.bw) && (o < nrows);
-                    if (DEBUG && valid)
-                        dbg_map[(int64_t)T.frame * dbg_map_frame_stride + L.map_off +
-                                (int64_t)(T.y0 + o) * L.nx + (T.x0 + j)] = score;
-                    const bool pred = valid && (score > T1);     // "exceeded"
-                    const unsigned mask = __ballot_sync(0xFFFFFFFFu, pred);
-                    if (mask) {
-                        uint32_t base = 0;
-                        const int leader = __ffs(mask) - 1;
-                        if (lane == leader) base = atomicAdd(&ctrl->n_cand, (uint32_t)__popc(mask));
-                        base = __shfl_sync(0xFFFFFFFFu, base, leader);
-                        if (pred) {
-                            const uint32_t idx = base + __popc(mask & ((1u << lane) - 1u));
-                            if (idx < cand_cap) {
-                                S1Cand c;
-                                c.frame = T.frame;
-                                c.level = T.level;
-                                c.pad = 0;
-                                c.ix = (int16_t)(T.x0 + j);
-                                c.iy = (int16_t)(T.y0 + o);
-                                c.s1 = score;
-                                cands[idx] = c;
-                            }
+                // even/odd partial sums: lane r3=0 finalises output 2v-8 (its acc[0] + the odd
+                // lane's carry), lane r3=1 output 2v-7 (its acc[0] + the even lane's acc[1])
+                float fin[2];
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    const float send = r3 ? carry[m] : acc3[m][1];
+                    fin[m] = acc3[m][0] + __shfl_xor_sync(0xFFFFFFFFu, send, 1);
+                    carry[m] = acc3[m][1];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc3[m][i] = acc3[m][i + 2];
+                    acc3[m][4] = 0.f;
+                    acc3[m][5] = 0.f;
+                }
+                const int o = 2 * v - 8 + r3;                // finished window row (task-relative)
+                const float a0 = act(fin[0] + W.b3[0]);
+                const float a1 = act(fin[1] + W.b3[1]);
+                const float score = act(fmaf(W.w4[1], a1, fmaf(W.w4[0], a0, W.b4)));
+                const bool valid = (o >= 0) && (o < nrows) && (j3 < T.bw);
+                if (DEBUG && valid)
+                    dbg_map[(int64_t)T.frame * dbg_map_frame_stride + L.map_off +
+                            (int64_t)(T.y0 + o) * L.nx + (T.x0 + j3)] = score;
+                const bool pred = valid && (score > T1);             // "exceeded"
+                const unsigned mask = __ballot_sync(0xFFFFFFFFu, pred);
+                if (mask) {
+                    uint32_t base = 0;
+                    const int leader = __ffs(mask) - 1;
+                    if (lane == leader) base = atomicAdd(&ctrl->n_cand, (uint32_t)__popc(mask));
+                    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+                    if (pred) {
+                        const uint32_t idx = base + __popc(mask & ((1u << lane) - 1u));
+                        if (idx < cand_cap) {
+                            S1Cand cd;
+                            cd.frame = T.frame;
+                            cd.level = T.level;
+                            cd.pad = 0;
+                            cd.ix = (int16_t)(T.x0 + j3);
+                            cd.iy = (int16_t)(T.y0 + o);
+                            cd.s1 = score;
+                            cands[idx] = cd;
                         }
                     }
                 }
-#pragma unroll
-                for (int m = 0; m < 2; ++m) {
-#pragma unroll
-                    for (int i = 0; i < 5; ++i) acc3[m][i] = acc3[m][i + 1];
-                    acc3[m][5] = 0.f;
-                }
             }
+#ifdef S1_PROFILE
+            const long long t_bar0 = clock64();
+#endif
             __syncthreads();
+#ifdef S1_PROFILE
+            if (lane == 0) atomicAdd(&ctrl->pad[0], (uint32_t)((clock64() - t_bar0) >> 6));
+#endif
         }
     }
 }
 
-constexpr int kNT = 128;
-
 template <bool DEBUG>
-void launch_impl(const Cnn1W& w, float T1, const uint8_t* levels, int64_t lfs,
-                 const LevelInfo* d_levels, const S1Task* d_tasks, int n_tasks, S1Cand* cands,
-                 uint32_t cand_cap, Ctrl* ctrl, float* dbg_map, int64_t dbg_fs, int sm_count,
-                 cudaStream_t s)
+int occupancy()
 {
-    using C = Cfg<kNT>;
-    const size_t smem = sizeof(float) * C::SMEM_FLOATS;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(stage1_kernel<kNT, DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        attr_set = true;
-    }
+    const size_t smem = sizeof(float) * SMEM_FLOATS;
+    cudaFuncSetAttribute(stage1_kernel<DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stage1_kernel<kNT, DEBUG>, kNT, smem);
-    if (occ < 1) occ = 1;
-    int grid = sm_count * occ;
-    if (grid > n_tasks) grid = n_tasks;
-    if (grid < 1) return;
-    stage1_kernel<kNT, DEBUG><<<grid, kNT, smem, s>>>(w, T1, levels, lfs, d_levels, d_tasks, n_tasks,
-                                                      cands, cand_cap, ctrl, dbg_map, dbg_fs);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stage1_kernel<DEBUG>, NT, smem);
+    return occ < 1 ? 1 : occ;
 }
 
 }  // namespace
 
-int stage1_band_width() { return Cfg<kNT>::TW; }
+int stage1_band_width() { return TW; }
+
+int stage1_grid(int sm_count)
+{
+    // the production and debug instantiations must share one schedule
+    return sm_count * std::min(occupancy<false>(), occupancy<true>());
+}
+
+int stage1_task_cost(int nrows) { return (nrows + 7) / 2 + 1 + 2; }   // super-steps + prologue
 
 void launch_stage1(const Cnn1W& w, float T1, const uint8_t* levels, int64_t level_frame_stride,
-                   const LevelInfo* d_levels, const S1Task* d_tasks, int n_tasks, S1Cand* cands,
-                   uint32_t cand_cap, Ctrl* ctrl, float* dbg_map, int64_t dbg_map_frame_stride,
-                   int sm_count, cudaStream_t s)
+                   const LevelInfo* d_levels, const S1Task* d_tasks, const int32_t* d_cta_first,
+                   int grid, S1Cand* cands, uint32_t cand_cap, Ctrl* ctrl, float* dbg_map,
+                   int64_t dbg_map_frame_stride, cudaStream_t s)
 {
-    if (n_tasks <= 0) return;
-    if (dbg_map)
-        launch_impl<true>(w, T1, levels, level_frame_stride, d_levels, d_tasks, n_tasks, cands,
-                          cand_cap, ctrl, dbg_map, dbg_map_frame_stride, sm_count, s);
-    else
-        launch_impl<false>(w, T1, levels, level_frame_stride, d_levels, d_tasks, n_tasks, cands,
-                           cand_cap, ctrl, nullptr, 0, sm_count, s);
+    if (grid <= 0) return;
+    const size_t smem = sizeof(float) * SMEM_FLOATS;
+    if (dbg_map) {
+        cudaFuncSetAttribute(stage1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        stage1_kernel<true><<<grid, NT, smem, s>>>(w, T1, levels, level_frame_stride, d_levels, d_tasks,
+                                                   d_cta_first, cands, cand_cap, ctrl, dbg_map,
+                                                   dbg_map_frame_stride);
+    } else {
+        cudaFuncSetAttribute(stage1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        stage1_kernel<false><<<grid, NT, smem, s>>>(w, T1, levels, level_frame_stride, d_levels, d_tasks,
+                                                    d_cta_first, cands, cand_cap, ctrl, nullptr, 0);
+    }
 }
 
 }  // namespace ccnn
