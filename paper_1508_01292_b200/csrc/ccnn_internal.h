@@ -27,7 +27,9 @@ struct __align__(16) Cnn1W {   // 797 weights + re-arranged copies for the stage
     float w4[2], b4;
 };
 template <int A, int B, int C>
-struct SelNetW {               // CNN2: <16,6,2>, CNN3: <2,2,25>
+struct __align__(16) SelNetW { // CNN2: <16,6,2>, CNN3: <2,2,25>
+    static constexpr int W2V = (B * 9 + 3) / 4 * 4;
+    float w2v[A][W2V];         // layer 2 per input map a: [b*9 + ky*3 + kx], float4 blocks
     float w1[A][16], b1[A];
     float w2[B][A][9], b2[B];
     float w3[C][B][56], b3[C]; // [out][in][ky*7+kx], 7 wide x 8 tall
@@ -44,7 +46,7 @@ struct LevelInfo {             // one pyramid level (same for every frame of a b
     int32_t nx, ny;            // window grid
     int32_t map_off;           // offset of the level in one frame's dense stage-1 map (debug)
     int32_t tab_off;           // offset of the level's x table (lw entries) then y table (lh)
-    int32_t row0;              // first row of the level in the concatenation of all levels
+    int32_t row0;              // rows of all earlier levels (pyramid grid: one CTA per level row)
 };
 struct S1Task {                // one stage-1 CTA task: a band of windows on one level
     int32_t frame;
@@ -82,6 +84,7 @@ struct Ctrl {
     uint32_t pad[7];
 };
 
+constexpr int kMaxLevels = 256;   // pyramid levels per frame (scale_step 1.02 spans 11 octaves)
 constexpr int kNmsCap = 4096;  // raw boxes per frame handled by one NMS CTA
 
 // ---- launchers (stream-ordered, no sync) ----

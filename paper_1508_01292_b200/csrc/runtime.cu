@@ -169,19 +169,25 @@ void unpack_sel(const float* p, SelNetW<A, B, C>& o)
     std::memcpy(o.b3, p, sizeof(o.b3)); p += C;
     std::memcpy(o.w4, p, sizeof(o.w4)); p += C;
     o.b4 = *p;
+    for (int a = 0; a < A; ++a)
+        for (int k = 0; k < SelNetW<A, B, C>::W2V; ++k)
+            o.w2v[a][k] = k < B * 9 ? o.w2[k / 9][a][k % 9] : 0.f;
 }
 
 int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 // O2 sampling table entry: s = (d + 0.5)/sigma - 0.5, clamp [0, n-1], i0 = floor(s),
-// a = floor((s - i0) * 2048 + 0.5); packed i0 | a << 16.
+// i1 = min(i0 + 1, n - 1), a = floor((s - i0) * 2048 + 0.5); packed i0 | a << 16.
+// For n >= 2 the clamped edge (i0 = n-1, a = 0) is re-encoded as (i0 = n-2, a = 2048):
+// p[n-2]*0 + p[n-1]*2048 == p[n-1]*2048 exactly, so the kernel may always use i0 + 1.
 uint32_t sample_entry(int d, double sigma, int n)
 {
     double s = ((double)d + 0.5) / sigma - 0.5;
     if (s < 0.0) s = 0.0;
     if (s > (double)(n - 1)) s = (double)(n - 1);
-    const int f = (int)std::floor(s);
-    const int a = (int)std::floor((s - (double)f) * 2048.0 + 0.5);
+    int f = (int)std::floor(s);
+    int a = (int)std::floor((s - (double)f) * 2048.0 + 0.5);
+    if (n >= 2 && f == n - 1) { f = n - 2; a = 2048; }
     return (uint32_t)f | ((uint32_t)a << 16);
 }
 
@@ -194,7 +200,7 @@ void build_plan(ccnn_ctx* c, int n, int W, int H, int min_face, float scale_step
     const double sf = (double)scale_step;
     double s = (double)kWinW / (double)min_face;
     int64_t off = 0, map_off = 0;
-    int row0 = 0;
+    int64_t row0 = 0;
     c->windows_per_frame = 0;
     while (true) {
         const int lw = (int)std::floor((double)W * s);
@@ -210,7 +216,7 @@ void build_plan(ccnn_ctx* c, int n, int W, int H, int min_face, float scale_step
         L.ny = (lh - kWinH) / kStep + 1;
         L.map_off = (int32_t)map_off;
         L.tab_off = (int32_t)c->tabs.size();
-        L.row0 = row0;
+        L.row0 = (int32_t)row0;                      // rows of earlier levels
         for (int x = 0; x < lw; ++x) c->tabs.push_back(sample_entry(x, s, W));
         for (int y = 0; y < lh; ++y) c->tabs.push_back(sample_entry(y, s, H));
         off += round_up((int64_t)L.pitch * lh, 256);
@@ -392,6 +398,11 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
     const bool replan = !(key == ctx->key);
     if (replan) build_plan(ctx, n, w, h, min_face, scale_step);
     const int L = (int)ctx->levels.size();
+    if (L > kMaxLevels) {
+        ctx->key = PlanKey{};
+        return fail(ctx, CCNN_E_ARG, "more than 256 pyramid levels (scale_step too close to 1)");
+    }
+
     if (stats) {
         std::memset(stats, 0, sizeof(*stats));
         stats->windows = ctx->windows_per_frame * n;

@@ -9,12 +9,17 @@
 // (51/35 x 55/39 about the window centre), the fixed-point bilinear sampling, the
 // round-half-up equalisation, K pooled over both orientations and the raw box.
 //
-// B200 design: a persistent kernel (grid = SMs x occupancy) drains the survivor queue
-// with a dynamic atomic counter -- the on-device form of the paper's asynchronous
-// selective unit.  One CTA per candidate: patch geometry in IEEE double
-// (explicit _rn intrinsics: never contracted, bit-identical to the oracle), integer
-// sampling/histogram/equalisation, then both orientations of CNN2 (and CNN3 when the
-// rule needs it) in fp32 with weights as constant-bank kernel parameters.
+// B200 design: a persistent kernel (grid = SMs x 2) drains the survivor queue with a
+// dynamic atomic counter -- the on-device form of the paper's asynchronous selective unit
+// (P:125-131).  One 288-thread CTA per candidate:
+//  * patch geometry in IEEE double with explicit _rn intrinsics (never contracted,
+//    bit-identical to the oracle); integer sampling, histogram and equalisation;
+//  * only the equalised patch E is stored; the mirrored orientation M(x,y) = E(50-x,y)
+//    is read through mirrored addresses by layer 1 (no second image, no flipped weights);
+//  * every layer's work is split over data (orientation x position [x map half]) so the
+//    weights a warp uses are warp-uniform constant-bank kernel parameters; planes are
+//    stored even/odd column de-interleaved so the stride-2 reads are conflict-free;
+//  * CNN3 runs only when the rule needs it (P:99 early stop).
 #include <type_traits>
 
 #include "ccnn_internal.h"
@@ -22,8 +27,11 @@
 namespace ccnn {
 namespace {
 
-constexpr int kSelThreads = 256;
-constexpr int kImgW = 52;                   // padded 51-wide patch rows
+constexpr int kSelThreads = 288;            // 9 warps: layer-2 items (264) in one round
+constexpr int kImgRS = 56;                  // patch row: even cols [0,26), odd cols [28,53)
+constexpr int kImgOdd = 28;
+constexpr int kP1RS = 24;                   // pooled L1 row (24 wide): even [0,12), odd [12,24)
+constexpr int kP1Odd = 12;
 
 __device__ __forceinline__ float act(float x)      // Eq. 1, see stage1.cu
 {
@@ -51,16 +59,19 @@ struct SelSmem {
     int hist[256];
     uint8_t lut[256];
     uint8_t patch[kPatchN + 3];
-    float img[2][kPatchH][kImgW];           // E and mirrored M, normalised (O3)
-    float p2[2][6][12][11];                 // pooled layer 2 (B <= 6 maps) [orient][map][y][x]
+    float img[kPatchH][kImgRS];             // E, normalised (O3), columns de-interleaved
+    float p2[2][6][12][12];                 // pooled layer 2 [orient][map][y][x]
+    float l3[25][2][25];                    // layer-3 activations [map][orient][cell]
     float resp[2][kResp];
     float wmax[kSelThreads / 32];
     int cand;
 };
+constexpr size_t kP1Floats = 2 * 16 * 26 * kP1RS;   // pooled layer 1 [orient][map][y][row]
 
-// pooled layer 1 lives after SelSmem: [2][A][26][24]
-template <int A>
-constexpr int p1_floats() { return 2 * A * 26 * 24; }
+__device__ __forceinline__ float img_at(const SelSmem& sm, int y, int x)
+{
+    return sm.img[y][(x & 1) ? kImgOdd + (x >> 1) : (x >> 1)];
+}
 
 // One selective CNN (architecture R: C4x4 1->A, P, C3x3 A->B, P, C7x8 B->C, C1x1 C->1,
 // Eq. 1 after every conv) on both orientations: 51x55 -> 2 x 5x5 responses in sm.resp.
@@ -68,98 +79,139 @@ template <int A, int B, int C>
 __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
 {
     const int tid = threadIdx.x;
-    // ---- layer 1: conv4x4 1->A, pool, act -> p1[o][a][26][24]; item = pooled position ----
-    for (int it = tid; it < 2 * 26 * 24; it += kSelThreads) {
-        const int o = it / (26 * 24), rem = it % (26 * 24), py0 = rem / 24, px0 = rem % 24;
+    // ---- layer 1: conv4x4 1->A, pool, act; item = (map group, orientation, pooled pos) ----
+    constexpr int G1 = (A >= 16) ? 8 : A;           // maps per item
+    constexpr int NG1 = A / G1;                     // 1248 = 39 warps of items per group
+    for (int it = tid; it < NG1 * 1248; it += kSelThreads) {
+        const int g = it / 1248, pos = it - g * 1248;
+        const int o = pos / 624, rem = pos - o * 624, py0 = rem / 24, px0 = rem - py0 * 24;
         float x[5][5];
+        if (o == 0) {
 #pragma unroll
-        for (int r = 0; r < 5; ++r)
+            for (int r = 0; r < 5; ++r)
 #pragma unroll
-            for (int c = 0; c < 5; ++c) x[r][c] = sm.img[o][2 * py0 + r][2 * px0 + c];
+                for (int c = 0; c < 5; ++c) x[r][c] = img_at(sm, 2 * py0 + r, 2 * px0 + c);
+        } else {                                    // M(x, y) = E(50 - x, y)
 #pragma unroll
-        for (int a = 0; a < A; ++a) {
-            float m = -INFINITY;
+            for (int r = 0; r < 5; ++r)
 #pragma unroll
-            for (int py = 0; py < 2; ++py)
+                for (int c = 0; c < 5; ++c) x[r][c] = img_at(sm, 2 * py0 + r, 50 - 2 * px0 - c);
+        }
+        auto body = [&](auto M0c) {
+            constexpr int M0 = decltype(M0c)::value;
 #pragma unroll
-                for (int px = 0; px < 2; ++px) {
-                    float s = W.b1[a];
+            for (int a = 0; a < G1; ++a) {
+                float s[4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    s[p] = W.b1[M0 + a];
 #pragma unroll
                     for (int ky = 0; ky < 4; ++ky)
 #pragma unroll
                         for (int kx = 0; kx < 4; ++kx)
-                            s = fmaf(W.w1[a][ky * 4 + kx], x[py + ky][px + kx], s);
-                    m = fmaxf(m, s);
+                            s[p] = fmaf(W.w1[M0 + a][ky * 4 + kx], x[(p >> 1) + ky][(p & 1) + kx], s[p]);
                 }
-            p1[((o * A + a) * 26 + py0) * 24 + px0] = act(m);   // pool then act (monotone)
+                const int col = (px0 & 1) ? kP1Odd + (px0 >> 1) : (px0 >> 1);
+                p1[((o * A + M0 + a) * 26 + py0) * kP1RS + col] =
+                    act(fmaxf(fmaxf(s[0], s[1]), fmaxf(s[2], s[3])));   // pool then act
+            }
+        };
+        if constexpr (NG1 == 1) body(std::integral_constant<int, 0>{});
+        else {
+            static_assert(NG1 == 2, "map groups");
+            if (g == 0) body(std::integral_constant<int, 0>{});      // warp-uniform branch
+            else body(std::integral_constant<int, 8>{});
         }
     }
     __syncthreads();
-    // ---- layer 2: conv3x3 A->B, pool, act -> p2[o][b][12][11]; item = (map pair, position) ----
-    constexpr int G = (B >= 2) ? 2 : 1, NG = B / G;
-    static_assert(B % G == 0, "map groups");
-    for (int it = tid; it < NG * 2 * 12 * 11; it += kSelThreads) {
-        const int g = it / (2 * 12 * 11), rem = it % (2 * 12 * 11);
-        const int o = rem / 132, pos = rem % 132, py0 = pos / 11, px0 = pos % 11;
-        auto body = [&](auto Bc) {
-            constexpr int B0 = decltype(Bc)::value;
-            float s[G][4];
+    // ---- layer 2: conv3x3 A->B, pool, act; item = (orientation, pooled position), all maps ----
+    if (tid < 2 * 132) {
+        const int o = tid / 132, pos = tid - o * 132, py0 = pos / 11, px0 = pos - py0 * 11;
+        float s[B][4];
 #pragma unroll
-            for (int b = 0; b < G; ++b)
+        for (int b = 0; b < B; ++b)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) s[b][k] = W.b2[B0 + b];
+            for (int k = 0; k < 4; ++k) s[b][k] = W.b2[b];
+#pragma unroll 1
+        for (int a = 0; a < A; ++a) {               // uniform counter: LDCU [UR+imm]
+            const float* in = p1 + ((o * A + a) * 26 + 2 * py0) * kP1RS;
+            float v[4][4];
 #pragma unroll
-            for (int a = 0; a < A; ++a) {
-                const float* in = p1 + ((o * A + a) * 26 + 2 * py0) * 24 + 2 * px0;
-                float v[4][4];
+            for (int r = 0; r < 4; ++r) {
+                v[r][0] = in[r * kP1RS + px0];
+                v[r][1] = in[r * kP1RS + kP1Odd + px0];
+                v[r][2] = in[r * kP1RS + px0 + 1];
+                v[r][3] = in[r * kP1RS + kP1Odd + px0 + 1];
+            }
+            constexpr int NV = SelNetW<A, B, C>::W2V;
+            float wv[NV];
+            const float4* w4p = reinterpret_cast<const float4*>(W.w2v[a]);
 #pragma unroll
-                for (int r = 0; r < 4; ++r)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) v[r][c] = in[r * 24 + c];
-#pragma unroll
-                for (int b = 0; b < G; ++b)
-#pragma unroll
-                    for (int py = 0; py < 2; ++py)
-#pragma unroll
-                        for (int px = 0; px < 2; ++px)
-#pragma unroll
-                            for (int ky = 0; ky < 3; ++ky)
-#pragma unroll
-                                for (int kx = 0; kx < 3; ++kx)
-                                    s[b][py * 2 + px] = fmaf(W.w2[B0 + b][a][ky * 3 + kx],
-                                                             v[py + ky][px + kx], s[b][py * 2 + px]);
+            for (int k4 = 0; k4 < NV / 4; ++k4) {
+                const float4 t4 = w4p[k4];
+                wv[4 * k4] = t4.x; wv[4 * k4 + 1] = t4.y; wv[4 * k4 + 2] = t4.z; wv[4 * k4 + 3] = t4.w;
             }
 #pragma unroll
-            for (int b = 0; b < G; ++b)
-                sm.p2[o][B0 + b][py0][px0] =
-                    act(fmaxf(fmaxf(s[b][0], s[b][1]), fmaxf(s[b][2], s[b][3])));
-        };
-        if constexpr (NG == 1) body(std::integral_constant<int, 0>{});
-        else if constexpr (NG == 3) {
-            if (g == 0) body(std::integral_constant<int, 0>{});
-            else if (g == 1) body(std::integral_constant<int, 2>{});
-            else body(std::integral_constant<int, 4>{});
-        } else {
-            static_assert(NG == 1 || NG == 3, "unsupported B");
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+                for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+                    for (int kx = 0; kx < 3; ++kx) {
+                        const float w = wv[b * 9 + ky * 3 + kx];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            s[b][k] = fmaf(w, v[(k >> 1) + ky][(k & 1) + kx], s[b][k]);
+                    }
         }
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+            sm.p2[o][b][py0][px0] = act(fmaxf(fmaxf(s[b][0], s[b][1]), fmaxf(s[b][2], s[b][3])));
     }
     __syncthreads();
-    // ---- layer 3 (C7x8 B->C, act) + layer 4 (C1x1 C->1, act); item = (orientation, cell) ----
-    if (tid < 2 * kResp) {
-        const int o = tid / kResp, cell = tid % kResp, y = cell / 5, x = cell % 5;
-        float r = W.b4;
-#pragma unroll 1
-        for (int c = 0; c < C; ++c) {
-            float s = W.b3[c];
+    // ---- layer 3: conv7x8 B->C, act; item = (map, orientation, cell) ----
+    if constexpr (C == 2) {
+        if (tid < 128) {                            // map = warp pair -> warp-uniform weights
+            const int m = tid >> 6, idx = tid & 63;
+            if (idx < 50) {
+                const int o = idx / 25, cell = idx - o * 25, y = cell / 5, x = cell - y * 5;
+                auto body = [&](auto Mc) {
+                    constexpr int M = decltype(Mc)::value;
+                    float s = W.b3[M];
+#pragma unroll
+                    for (int b = 0; b < B; ++b)
+#pragma unroll
+                        for (int ky = 0; ky < 8; ++ky)
+#pragma unroll
+                            for (int kx = 0; kx < 7; ++kx)
+                                s = fmaf(W.w3[M][b][ky * 7 + kx], sm.p2[o][b][y + ky][x + kx], s);
+                    sm.l3[M][o][cell] = act(s);
+                };
+                if (m == 0) body(std::integral_constant<int, 0>{});
+                else body(std::integral_constant<int, 1>{});
+            }
+        }
+    } else {
+        for (int it = tid; it < C * 50; it += kSelThreads) {
+            const int m = it / 50, idx = it - m * 50;
+            const int o = idx / 25, cell = idx - o * 25, y = cell / 5, x = cell - y * 5;
+            float s = W.b3[m];
 #pragma unroll
             for (int b = 0; b < B; ++b)
 #pragma unroll
                 for (int ky = 0; ky < 8; ++ky)
 #pragma unroll
                     for (int kx = 0; kx < 7; ++kx)
-                        s = fmaf(W.w3[c][b][ky * 7 + kx], sm.p2[o][b][y + ky][x + kx], s);
-            r = fmaf(W.w4[c], act(s), r);
+                        s = fmaf(W.w3[m][b][ky * 7 + kx], sm.p2[o][b][y + ky][x + kx], s);
+            sm.l3[m][o][cell] = act(s);
         }
+    }
+    __syncthreads();
+    // ---- layer 4: C1x1 C->1, act ----
+    if (tid < 2 * kResp) {
+        const int o = tid / kResp, cell = tid - o * kResp;
+        float r = W.b4;
+#pragma unroll
+        for (int c = 0; c < C; ++c) r = fmaf(W.w4[c], sm.l3[c][o][cell], r);
         sm.resp[o][cell] = act(r);
     }
     __syncthreads();
@@ -204,11 +256,11 @@ __global__ void __launch_bounds__(kSelThreads, 2) selective_kernel(
                 sm.rowy[v] = bilin_coord(__dsub_rn(__dadd_rn(ry, t), 0.5), Hd);
             }
         }
-        sm.hist[tid] = 0;                       // kSelThreads == 256 bins
+        if (tid < 256) sm.hist[tid] = 0;
         __syncthreads();
         // ---- O2 fixed-point bilinear sampling from the ORIGINAL frame + histogram ----
         for (int k = tid; k < kPatchN; k += kSelThreads) {
-            const int v = k / kPatchW, u = k % kPatchW;
+            const int v = k / kPatchW, u = k - v * kPatchW;
             const uint32_t xt = sm.colx[u], yt = sm.rowy[v];
             const uint32_t x0 = xt & 0xFFFFu, ax = xt >> 16, y0 = yt & 0xFFFFu, ay = yt >> 16;
             const uint32_t x1 = min(x0 + 1u, (uint32_t)(Wd - 1)), y1 = min(y0 + 1u, (uint32_t)(Hd - 1));
@@ -250,12 +302,11 @@ __global__ void __launch_bounds__(kSelThreads, 2) selective_kernel(
             }
         }
         __syncthreads();
-        // ---- E and mirrored M, normalised to [-1, 1] (O3) ----
+        // ---- E normalised to [-1, 1] (O3), columns de-interleaved ----
         for (int k = tid; k < kPatchN; k += kSelThreads) {
-            const int v = k / kPatchW, u = k % kPatchW;
-            const float e = fmaf((float)sm.lut[sm.patch[k]], 1.0f / 127.5f, -1.0f);
-            sm.img[0][v][u] = e;
-            sm.img[1][v][kPatchW - 1 - u] = e;
+            const int v = k / kPatchW, u = k - v * kPatchW;
+            sm.img[v][(u & 1) ? kImgOdd + (u >> 1) : (u >> 1)] =
+                fmaf((float)sm.lut[sm.patch[k]], 1.0f / 127.5f, -1.0f);
         }
         __syncthreads();
 
@@ -264,28 +315,26 @@ __global__ void __launch_bounds__(kSelThreads, 2) selective_kernel(
         float r2v = 0.f, r3v = 0.f;
         if (tid < 2 * kResp) r2v = sm.resp[tid / kResp][tid % kResp];
         const int K2 = __syncthreads_count(tid < 2 * kResp && r2v > sp.T2a);
-        float best = -INFINITY;
-        // block max of the responses of the last net evaluated (warp 0 + 1 hold them)
+        // block max of the responses of the last net evaluated (threads < 50 hold them)
         auto block_max = [&](float v) {
-            float* wm = sm.wmax;
             float m = (tid < 2 * kResp) ? v : -INFINITY;
 #pragma unroll
             for (int d = 16; d >= 1; d >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, d));
-            if ((tid & 31) == 0) wm[tid >> 5] = m;
+            if ((tid & 31) == 0) sm.wmax[tid >> 5] = m;
             __syncthreads();
-            float r = wm[0];
+            float r = sm.wmax[0];
 #pragma unroll
-            for (int k = 1; k < kSelThreads / 32; ++k) r = fmaxf(r, wm[k]);
+            for (int k = 1; k < kSelThreads / 32; ++k) r = fmaxf(r, sm.wmax[k]);
             __syncthreads();
             return r;
         };
         const bool stop = (sp.rule == 0) ? (K2 == 0) : (K2 >= sp.Tnn);   // P:99 / S:358
         int K3 = 0, delta, ran3 = 0;
+        float best;
         if (stop) {
             delta = (sp.rule == 0) ? 0 : 1;
             best = block_max(r2v);
         } else {
-            // CNN3 reuses img; responses of CNN2 are kept in registers (r2v)
             run_net<2, 2, 25>(W3, sm, p1);
             if (tid < 2 * kResp) r3v = sm.resp[tid / kResp][tid % kResp];
             K3 = __syncthreads_count(tid < 2 * kResp && r3v > sp.T2b);
@@ -324,7 +373,7 @@ __global__ void __launch_bounds__(kSelThreads, 2) selective_kernel(
 
 size_t selective_smem_bytes()
 {
-    return ((sizeof(SelSmem) + 15) & ~size_t(15)) + sizeof(float) * p1_floats<16>();
+    return ((sizeof(SelSmem) + 15) & ~size_t(15)) + sizeof(float) * kP1Floats;
 }
 
 void launch_selective(const Cnn2W& w2, const Cnn3W& w3, SelParams sp, const uint8_t* frames,
