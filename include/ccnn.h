@@ -125,6 +125,11 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
                 int frames_on_device, int min_face, float scale_step,
                 ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes, ccnn_stats* stats);
 
+/* Copy the boxes of the last ccnn_detect on ctx (also valid after it returned
+ * CCNN_E_CAPACITY, so a caller can fetch the result without detecting again).
+ * *n_boxes = the number of boxes; CCNN_E_CAPACITY if box_cap < *n_boxes. */
+int ccnn_last_boxes(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes);
+
 void ccnn_destroy(ccnn_ctx* ctx);
 
 /* Message of the last failing call on ctx ("" if none; static text if ctx is NULL). */

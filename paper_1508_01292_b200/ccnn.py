@@ -19,7 +19,8 @@ CCNN_E_CAPACITY, CCNN_E_QUEUE, CCNN_E_CUDA, CCNN_E_STATE = -4, -5, -6, -7
 CCNN_DEBUG_LEVELS, CCNN_DEBUG_STAGE1 = 1, 2
 
 # every entry point declared in include/ccnn.h
-EXPORTS = ("ccnn_create", "ccnn_set_stream", "ccnn_detect", "ccnn_destroy", "ccnn_last_error",
+EXPORTS = ("ccnn_create", "ccnn_set_stream", "ccnn_detect", "ccnn_last_boxes", "ccnn_destroy",
+           "ccnn_last_error",
            "ccnn_abi_version", "ccnn_set_debug", "ccnn_debug_levels", "ccnn_debug_level",
            "ccnn_debug_stage1_map", "ccnn_debug_candidates", "ccnn_debug_counters")
 
@@ -91,6 +92,7 @@ def load():
     L.ccnn_detect.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64,
                               C.c_int, C.c_int, C.c_float, _P(Box), C.c_int64, _P(C.c_int64),
                               _P(Stats)]
+    L.ccnn_last_boxes.argtypes = [C.c_void_p, _P(Box), C.c_int64, _P(C.c_int64)]
     L.ccnn_destroy.argtypes = [C.c_void_p]
     L.ccnn_destroy.restype = None
     L.ccnn_last_error.argtypes = [C.c_void_p]
@@ -127,6 +129,7 @@ class Detector:
             raise CcnnError(rc, "ccnn_create failed")
         self.h = h
         self.last_stats = None
+        self._cap = 1024
 
     def close(self):
         if getattr(self, "h", None):
@@ -176,19 +179,18 @@ class Detector:
             keep = a
         if stream is not None:
             self.set_stream(stream)
-        cap = box_cap if box_cap is not None else max(1024, 64 * n)
+        cap = box_cap if box_cap is not None else max(self._cap, 64 * n)
         nb = C.c_int64()
         st = Stats()
-        while True:
+        out = np.zeros(cap, BOX_DTYPE)
+        rc = L.ccnn_detect(self.h, C.c_void_p(ptr), n, W, H, pitch, on_device, min_face,
+                           scale_step, out.ctypes.data_as(_P(Box)), cap, C.byref(nb), C.byref(st))
+        if rc == CCNN_E_CAPACITY and box_cap is None:      # fetch, do not detect again
+            cap = int(nb.value)
+            self._cap = max(self._cap, cap)
             out = np.zeros(cap, BOX_DTYPE)
-            rc = L.ccnn_detect(self.h, C.c_void_p(ptr), n, W, H, pitch, on_device, min_face,
-                               scale_step, out.ctypes.data_as(_P(Box)), cap, C.byref(nb),
-                               C.byref(st))
-            if rc == CCNN_E_CAPACITY and box_cap is None:
-                cap = int(nb.value)
-                continue
-            self._check(rc)
-            break
+            rc = L.ccnn_last_boxes(self.h, out.ctypes.data_as(_P(Box)), cap, C.byref(nb))
+        self._check(rc)
         del keep
         self.last_stats = dict(windows=st.windows, stage1=st.stage1, stage2=st.stage2,
                                stage3=st.stage3, nms=st.nms, ms=list(st.ms),

@@ -92,6 +92,7 @@ struct ccnn_ctx {
     // last detect
     int last_n = 0, last_W = 0, last_H = 0;
     uint32_t last_cands = 0;
+    uint32_t last_nout = 0;
     bool last_valid = false;
 };
 
@@ -414,6 +415,7 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
         *n_boxes = 0;
         ctx->key = key;
         ctx->last_cands = 0;
+        ctx->last_nout = 0;
         ctx->last_valid = true;
         return CCNN_OK;
     }
@@ -503,12 +505,29 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
         }
     }
     *n_boxes = hc.n_out;
+    ctx->last_nout = hc.n_out;
     if ((int64_t)hc.n_out > box_cap)
         return fail(ctx, CCNN_E_CAPACITY, "box_cap too small: need " + std::to_string(hc.n_out));
     if (hc.n_out) {
         static_assert(sizeof(OutBox) == sizeof(ccnn_box), "OutBox mirrors ccnn_box");
         CU(cudaMemcpyAsync(boxes, ctx->out.p, sizeof(OutBox) * hc.n_out, cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
+    }
+    return CCNN_OK;
+}
+
+int ccnn_last_boxes(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes)
+{
+    if (!ctx || !n_boxes || (box_cap > 0 && !boxes)) return CCNN_E_ARG;
+    if (!ctx->last_valid) return fail(ctx, CCNN_E_STATE, "no completed detect");
+    *n_boxes = ctx->last_nout;
+    if ((int64_t)ctx->last_nout > box_cap)
+        return fail(ctx, CCNN_E_CAPACITY, "box_cap too small: need " + std::to_string(ctx->last_nout));
+    if (ctx->last_nout) {
+        CU(cudaSetDevice(ctx->device));
+        CU(cudaMemcpyAsync(boxes, ctx->out.p, sizeof(OutBox) * ctx->last_nout, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
     }
     return CCNN_OK;
 }

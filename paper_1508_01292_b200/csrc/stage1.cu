@@ -55,7 +55,7 @@ constexpr int IN_ODD = NT + 4;          // odd input columns start inside a ring
 constexpr int IN_RS = 2 * NT + 8;       // input ring row stride (floats)
 constexpr int IN_RING = 12;             // rows 8v .. 8v+10 (+ 8v+11 .. 8v+18 after the mid barrier)
 constexpr int P1_ODD = NT / 2 + 16;     // odd P1 columns start (bank offset 16)
-constexpr int P1_RS = NT + 16;          // one (row, map) of the P1 ring
+constexpr int P1_RS = NT + 20;          // one (row, map) of the P1 ring (+4: L2 lane 63 reads [144])
 constexpr int P1_RING = 6;              // rows 4v-2 .. 4v+3
 constexpr int P2_RS = NT / 2 + 8;
 constexpr int P2_RING = 4;              // rows 2v-3 .. 2v
