@@ -249,21 +249,26 @@ def main():
         ms = float(t.item())
     clk = clocks.stop() if clocks else None
 
-    # ---- e2e: same call with the frames in pinned host memory (H2D inside the timed region)
+    # ---- e2e: the streaming public API (ccnn_submit / ccnn_collect) with the frames in
+    #      pinned HOST memory: every step copies its 265 MB H2D and reads its boxes back;
+    #      the copy of step k+1 overlaps the kernels of step k (two batches in flight) ----
     e2e_steps = args.e2e_steps or max(3, args.steps // 2)
     host = torch.from_numpy(frames).pin_memory()
     det.detect(host, cfg.min_face, cfg.scale_step)
     barrier()
+    t_e2e0 = time.perf_counter()
     h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     h0.record(stream)
     d2h = 0
-    for _ in range(e2e_steps):
-        b = det.detect(host, cfg.min_face, cfg.scale_step)
-        d2h += b.nbytes + 64
+    det.submit(host, cfg.min_face, cfg.scale_step, timed=False)
+    for k in range(1, e2e_steps):
+        det.submit(host, cfg.min_face, cfg.scale_step, timed=False)
+        d2h += det.collect().nbytes + 64
+    d2h += det.collect().nbytes + 64
     h1.record(stream)
     h1.synchronize()
     barrier()
-    ms_e2e = h0.elapsed_time(h1)
+    ms_e2e = max(h0.elapsed_time(h1), 1000.0 * (time.perf_counter() - t_e2e0) - 1.0)
     if dist is not None:
         t = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -125,8 +125,25 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
                 int frames_on_device, int min_face, float scale_step,
                 ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes, ccnn_stats* stats);
 
-/* Copy the boxes of the last ccnn_detect on ctx (also valid after it returned
- * CCNN_E_CAPACITY, so a caller can fetch the result without detecting again).
+/* Streaming form of ccnn_detect (a video stream).
+ * ccnn_submit enqueues one batch (same arguments as ccnn_detect) and returns at once: host
+ * frames are copied H2D on an internal copy stream into one of two per-ctx frame buffers,
+ * so the copy of batch k+1 overlaps the kernels of batch k; host frames must stay valid
+ * (and should be pinned) until the batch is collected; device frames until then too.
+ * At most two batches may be in flight (CCNN_E_STATE otherwise); timed != 0 records the
+ * per-stage events reported by ccnn_collect's stats.
+ * ccnn_collect waits for the OLDEST in-flight batch and returns its boxes exactly like
+ * ccnn_detect (including CCNN_E_CAPACITY + ccnn_last_boxes).  ccnn_detect = submit +
+ * collect and is refused while batches are in flight.  Do not change the stream while
+ * batches are in flight. */
+int ccnn_submit(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64_t pitch,
+                int frames_on_device, int min_face, float scale_step, int timed);
+int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes,
+                 ccnn_stats* stats);
+
+/* Copy the boxes of the last ccnn_detect / ccnn_collect on ctx (also valid after it
+ * returned CCNN_E_CAPACITY, so a caller can fetch the result without detecting again;
+ * valid until the next-but-one ccnn_submit reuses its output buffer).
  * *n_boxes = the number of boxes; CCNN_E_CAPACITY if box_cap < *n_boxes. */
 int ccnn_last_boxes(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes);
 

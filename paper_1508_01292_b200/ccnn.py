@@ -19,8 +19,8 @@ CCNN_E_CAPACITY, CCNN_E_QUEUE, CCNN_E_CUDA, CCNN_E_STATE = -4, -5, -6, -7
 CCNN_DEBUG_LEVELS, CCNN_DEBUG_STAGE1 = 1, 2
 
 # every entry point declared in include/ccnn.h
-EXPORTS = ("ccnn_create", "ccnn_set_stream", "ccnn_detect", "ccnn_last_boxes", "ccnn_destroy",
-           "ccnn_last_error",
+EXPORTS = ("ccnn_create", "ccnn_set_stream", "ccnn_detect", "ccnn_submit", "ccnn_collect",
+           "ccnn_last_boxes", "ccnn_destroy", "ccnn_last_error",
            "ccnn_abi_version", "ccnn_set_debug", "ccnn_debug_levels", "ccnn_debug_level",
            "ccnn_debug_stage1_map", "ccnn_debug_candidates", "ccnn_debug_counters")
 
@@ -93,6 +93,9 @@ def load():
                               C.c_int, C.c_int, C.c_float, _P(Box), C.c_int64, _P(C.c_int64),
                               _P(Stats)]
     L.ccnn_last_boxes.argtypes = [C.c_void_p, _P(Box), C.c_int64, _P(C.c_int64)]
+    L.ccnn_submit.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64,
+                              C.c_int, C.c_int, C.c_float, C.c_int]
+    L.ccnn_collect.argtypes = [C.c_void_p, _P(Box), C.c_int64, _P(C.c_int64), _P(Stats)]
     L.ccnn_destroy.argtypes = [C.c_void_p]
     L.ccnn_destroy.restype = None
     L.ccnn_last_error.argtypes = [C.c_void_p]
@@ -130,6 +133,7 @@ class Detector:
         self.h = h
         self.last_stats = None
         self._cap = 1024
+        self._inflight = []
 
     def close(self):
         if getattr(self, "h", None):
@@ -152,11 +156,8 @@ class Detector:
     def set_debug(self, flags):
         self._check(load().ccnn_set_debug(self.h, flags))
 
-    def detect(self, frames, min_face, scale_step, box_cap=None, stream=None):
-        """frames: torch uint8 tensor (n, H, W) on the ctx device or on the host, or a numpy
-        uint8 array (n, H, W).  Returns a numpy structured array of boxes (BOX_DTYPE)."""
-        L = load()
-        on_device = 0
+    def _frames(self, frames, stream):
+        """(ptr, n, H, W, pitch, on_device, keepalive) for a torch tensor or numpy array."""
         if hasattr(frames, "data_ptr"):                  # torch tensor
             import torch
             t = frames if frames.dim() == 3 else frames.unsqueeze(0)
@@ -164,19 +165,33 @@ class Detector:
             n, H, W = t.shape
             pitch = t.stride(1)
             assert t.stride(2) == 1 and t.stride(0) == H * pitch
-            ptr = t.data_ptr()
-            on_device = 1 if t.is_cuda else 0
             if t.is_cuda and stream is None:
                 stream = torch.cuda.current_stream(t.device).cuda_stream
-            keep = t
-        else:
-            a = np.ascontiguousarray(frames, np.uint8)
-            if a.ndim == 2:
-                a = a[None]
-            n, H, W = a.shape
-            pitch = W
-            ptr = a.ctypes.data
-            keep = a
+            return t.data_ptr(), n, H, W, pitch, 1 if t.is_cuda else 0, t, stream
+        a = np.ascontiguousarray(frames, np.uint8)
+        if a.ndim == 2:
+            a = a[None]
+        n, H, W = a.shape
+        return a.ctypes.data, n, H, W, W, 0, a, stream
+
+    def _result(self, rc, nb, st, box_cap, out):
+        L = load()
+        if rc == CCNN_E_CAPACITY and box_cap is None:      # fetch, do not detect again
+            cap = int(nb.value)
+            self._cap = max(self._cap, cap)
+            out = np.zeros(cap, BOX_DTYPE)
+            rc = L.ccnn_last_boxes(self.h, out.ctypes.data_as(_P(Box)), cap, C.byref(nb))
+        self._check(rc)
+        self.last_stats = dict(windows=st.windows, stage1=st.stage1, stage2=st.stage2,
+                               stage3=st.stage3, nms=st.nms, ms=list(st.ms),
+                               kernel_launches=st.kernel_launches)
+        return out[:nb.value].copy()
+
+    def detect(self, frames, min_face, scale_step, box_cap=None, stream=None):
+        """frames: torch uint8 tensor (n, H, W) on the ctx device or on the host, or a numpy
+        uint8 array (n, H, W).  Returns a numpy structured array of boxes (BOX_DTYPE)."""
+        L = load()
+        ptr, n, H, W, pitch, on_device, keep, stream = self._frames(frames, stream)
         if stream is not None:
             self.set_stream(stream)
         cap = box_cap if box_cap is not None else max(self._cap, 64 * n)
@@ -185,17 +200,31 @@ class Detector:
         out = np.zeros(cap, BOX_DTYPE)
         rc = L.ccnn_detect(self.h, C.c_void_p(ptr), n, W, H, pitch, on_device, min_face,
                            scale_step, out.ctypes.data_as(_P(Box)), cap, C.byref(nb), C.byref(st))
-        if rc == CCNN_E_CAPACITY and box_cap is None:      # fetch, do not detect again
-            cap = int(nb.value)
-            self._cap = max(self._cap, cap)
-            out = np.zeros(cap, BOX_DTYPE)
-            rc = L.ccnn_last_boxes(self.h, out.ctypes.data_as(_P(Box)), cap, C.byref(nb))
-        self._check(rc)
+        res = self._result(rc, nb, st, box_cap, out)
         del keep
-        self.last_stats = dict(windows=st.windows, stage1=st.stage1, stage2=st.stage2,
-                               stage3=st.stage3, nms=st.nms, ms=list(st.ms),
-                               kernel_launches=st.kernel_launches)
-        return out[:nb.value].copy()
+        return res
+
+    def submit(self, frames, min_face, scale_step, stream=None, timed=True):
+        """Enqueue one batch (ccnn_submit); the frames are kept alive until collect()."""
+        L = load()
+        ptr, n, H, W, pitch, on_device, keep, stream = self._frames(frames, stream)
+        if stream is not None:
+            self.set_stream(stream)
+        self._check(L.ccnn_submit(self.h, C.c_void_p(ptr), n, W, H, pitch, on_device, min_face,
+                                  scale_step, 1 if timed else 0))
+        self._inflight.append((keep, n))
+
+    def collect(self, box_cap=None):
+        """Boxes of the oldest submitted batch (ccnn_collect)."""
+        L = load()
+        keep, n = self._inflight[0]
+        cap = box_cap if box_cap is not None else max(self._cap, 64 * n)
+        nb = C.c_int64()
+        st = Stats()
+        out = np.zeros(cap, BOX_DTYPE)
+        rc = L.ccnn_collect(self.h, out.ctypes.data_as(_P(Box)), cap, C.byref(nb), C.byref(st))
+        self._inflight.pop(0)
+        return self._result(rc, nb, st, box_cap, out)
 
     # ---- test hooks ----
     def levels(self):

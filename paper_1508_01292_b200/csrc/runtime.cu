@@ -84,12 +84,27 @@ struct ccnn_ctx {
     int64_t map_frame_stride = 0;
     int64_t windows_per_frame = 0;
 
-    DevBuf frames, arena, d_levels, d_tasks, d_cta_first, d_tabs, cands, selout, dbg_resp, acc, ctrl, staging,
-        counts, out, dbg_map;
-    Ctrl* h_ctrl = nullptr;                 // pinned readback
-    cudaEvent_t ev[6] = {};
+    // shared by consecutive batches (their kernels are ordered on the compute stream)
+    DevBuf arena, d_levels, d_tasks, d_cta_first, d_tabs, cands, selout, dbg_resp, acc, staging,
+        counts, dbg_map;
 
-    // last detect
+    // per in-flight batch (ccnn_submit / ccnn_collect ping-pong, NEXT #2 streaming ingest)
+    struct Slot {
+        DevBuf frames;              // H2D destination (host input)
+        DevBuf ctrl, out;           // control block, compacted boxes
+        Ctrl* h_ctrl = nullptr;     // pinned readback of ctrl
+        cudaEvent_t ev[7] = {};     // h2d0, h2d1, c0, pyramid, stage1, selective, end
+        bool used = false;          // a batch has been enqueued on this slot before
+        int n = 0;
+        uint32_t cand_cap = 0;
+        int64_t windows = 0;
+        bool timed = false, empty = false;
+    } slot[2];
+    cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
+    int next_slot = 0, inflight = 0;
+
+    // last collected batch (test hooks, ccnn_last_boxes)
+    int last_slot = 0;
     int last_n = 0, last_W = 0, last_H = 0;
     uint32_t last_cands = 0;
     uint32_t last_nout = 0;
@@ -339,9 +354,14 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
     ctx->seg_rows_param = p->segment_rows;
     ctx->s1_grid = stage1_grid(ctx->sm_count);
     CU(cudaGetLastError());
-    CU(cudaMallocHost(&ctx->h_ctrl, sizeof(Ctrl)));
-    for (auto& e : ctx->ev) CU(cudaEventCreate(&e));
-    CU(ctx->ctrl.ensure(sizeof(Ctrl)));
+    for (auto& sl : ctx->slot) {
+        CU(cudaMallocHost(&sl.h_ctrl, sizeof(Ctrl)));
+        std::memset(sl.h_ctrl, 0, sizeof(Ctrl));
+        for (auto& e : sl.ev) CU(cudaEventCreate(&e));
+        CU(sl.ctrl.ensure(sizeof(Ctrl)));
+    }
+    CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
     *out = ctx;
     return CCNN_OK;
 }
@@ -364,24 +384,28 @@ void ccnn_destroy(ccnn_ctx* ctx)
 {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream); else cudaDeviceSynchronize();
-    for (DevBuf* b : {&ctx->frames, &ctx->arena, &ctx->d_levels, &ctx->d_tasks, &ctx->d_cta_first, &ctx->d_tabs,
-                      &ctx->cands, &ctx->selout, &ctx->dbg_resp, &ctx->acc, &ctx->ctrl,
-                      &ctx->staging, &ctx->counts, &ctx->out, &ctx->dbg_map})
+    cudaDeviceSynchronize();
+    for (DevBuf* b : {&ctx->arena, &ctx->d_levels, &ctx->d_tasks, &ctx->d_cta_first, &ctx->d_tabs,
+                      &ctx->cands, &ctx->selout, &ctx->dbg_resp, &ctx->acc, &ctx->staging, &ctx->counts,
+                      &ctx->dbg_map})
         b->release();
-    if (ctx->h_ctrl) cudaFreeHost(ctx->h_ctrl);
-    for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
+    for (auto& sl : ctx->slot) {
+        sl.frames.release();
+        sl.ctrl.release();
+        sl.out.release();
+        if (sl.h_ctrl) cudaFreeHost(sl.h_ctrl);
+        for (auto& e : sl.ev) if (e) cudaEventDestroy(e);
+    }
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
     delete ctx;
 }
 
-int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64_t pitch,
-                int frames_on_device, int min_face, float scale_step, ccnn_box* boxes,
-                int64_t box_cap, int64_t* n_boxes, ccnn_stats* stats)
+int ccnn_submit(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64_t pitch,
+                int frames_on_device, int min_face, float scale_step, int timed)
 {
     if (!ctx) return CCNN_E_ARG;
-    ctx->last_valid = false;
-    if (!frames || !n_boxes || (box_cap > 0 && !boxes))
-        return fail(ctx, CCNN_E_ARG, "NULL frames / n_boxes / boxes");
+    if (!frames) return fail(ctx, CCNN_E_ARG, "NULL frames");
     if (n <= 0 || n > ctx->max_batch) return fail(ctx, CCNN_E_ARG, "n out of [1, max_batch]");
     if (w < 1 || h < 1 || w > ctx->max_w || h > ctx->max_h)
         return fail(ctx, CCNN_E_ARG, "frame size out of [1, max_w] x [1, max_h]");
@@ -391,36 +415,39 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
         return fail(ctx, CCNN_E_ARG, "scale_step must be > 1 (S:227)");
     if ((double)kWinW / min_face * std::max(w, h) > 32000.0)
         return fail(ctx, CCNN_E_ARG, "level 0 too large (min_face too small for this frame)");
+    if (ctx->inflight >= 2) return fail(ctx, CCNN_E_STATE, "two batches in flight: ccnn_collect first");
     CU(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    const bool timing = stats != nullptr;
 
     PlanKey key{n, w, h, min_face, scale_step};
     const bool replan = !(key == ctx->key);
-    if (replan) build_plan(ctx, n, w, h, min_face, scale_step);
+    if (replan) {
+        CU(cudaStreamSynchronize(s));              // tables of an in-flight batch stay valid
+        build_plan(ctx, n, w, h, min_face, scale_step);
+    }
     const int L = (int)ctx->levels.size();
     if (L > kMaxLevels) {
         ctx->key = PlanKey{};
         return fail(ctx, CCNN_E_ARG, "more than 256 pyramid levels (scale_step too close to 1)");
     }
-
-    if (stats) {
-        std::memset(stats, 0, sizeof(*stats));
-        stats->windows = ctx->windows_per_frame * n;
-    }
-    ctx->last_n = n;
+    ccnn_ctx::Slot& sl = ctx->slot[ctx->next_slot];
+    sl.n = n;
+    sl.windows = ctx->windows_per_frame * n;
+    sl.timed = timed != 0;
+    sl.empty = (L == 0);                           // empty pyramid: not an error
     ctx->last_W = w;
     ctx->last_H = h;
-    if (L == 0) {                                  // empty pyramid: not an error
-        *n_boxes = 0;
+    if (sl.empty) {
         ctx->key = key;
-        ctx->last_cands = 0;
-        ctx->last_nout = 0;
-        ctx->last_valid = true;
+        sl.cand_cap = 0;
+        CU(cudaEventRecord(sl.ev[6], s));
+        ctx->next_slot ^= 1;
+        ctx->inflight++;
         return CCNN_OK;
     }
 
     const uint32_t cand_cap = (uint32_t)std::min<int64_t>((int64_t)ctx->queue_cap * n, 0x7FFFFFFF);
+    sl.cand_cap = cand_cap;
     CU(ctx->arena.ensure((size_t)ctx->level_frame_stride * n));
     CU(ctx->d_levels.ensure(sizeof(LevelInfo) * L));
     CU(ctx->d_tasks.ensure(sizeof(S1Task) * ctx->tasks.size()));
@@ -431,7 +458,7 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
     CU(ctx->acc.ensure(sizeof(AccBox) * cand_cap));
     CU(ctx->staging.ensure(sizeof(OutBox) * 2 * kNmsCap * (size_t)n));
     CU(ctx->counts.ensure(sizeof(int32_t) * n));
-    CU(ctx->out.ensure(sizeof(OutBox) * cand_cap));
+    CU(sl.out.ensure(sizeof(OutBox) * cand_cap));
     const bool dbg1 = (ctx->debug & CCNN_DEBUG_STAGE1) != 0;
     if (dbg1) {
         CU(ctx->dbg_map.ensure(sizeof(float) * ctx->map_frame_stride * n));
@@ -450,45 +477,83 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
     }
     ctx->key = key;
 
-    // ---- frames: device-resident, or H2D into the ctx buffer (host -> device boundary) ----
+    // ---- frames: device-resident, or H2D on the copy stream (host -> device boundary);
+    //      the copy of batch k+1 overlaps the kernels of batch k ----
     const uint8_t* dframes = frames;
     int64_t dpitch = pitch;
-    if (timing) CU(cudaEventRecord(ctx->ev[0], s));
     if (!frames_on_device) {
         dpitch = round_up(w, 16);
-        CU(ctx->frames.ensure((size_t)dpitch * h * n));
-        CU(cudaMemcpy2DAsync(ctx->frames.p, dpitch, frames, pitch, w, (size_t)h * n,
-                             cudaMemcpyHostToDevice, s));
-        dframes = ctx->frames.as<uint8_t>();
+        CU(sl.frames.ensure((size_t)dpitch * h * n));
+        // the previous batch of this slot (k-2) read these frames until its end event
+        if (sl.used) CU(cudaStreamWaitEvent(ctx->copy_stream, sl.ev[6], 0));
+        CU(cudaEventRecord(sl.ev[0], ctx->copy_stream));
+        CU(cudaMemcpy2DAsync(sl.frames.p, dpitch, frames, pitch, w, (size_t)h * n,
+                             cudaMemcpyHostToDevice, ctx->copy_stream));
+        CU(cudaEventRecord(sl.ev[1], ctx->copy_stream));
+        CU(cudaStreamWaitEvent(s, sl.ev[1], 0));
+        dframes = sl.frames.as<uint8_t>();
+    } else {
+        CU(cudaEventRecord(sl.ev[0], s));
+        CU(cudaEventRecord(sl.ev[1], s));
     }
     const int64_t fstride = dpitch * h;
-    CU(cudaMemsetAsync(ctx->ctrl.p, 0, sizeof(Ctrl), s));
-    if (timing) CU(cudaEventRecord(ctx->ev[1], s));
+    Ctrl* dctrl = sl.ctrl.as<Ctrl>();
+    CU(cudaMemsetAsync(dctrl, 0, sizeof(Ctrl), s));
+    CU(cudaEventRecord(sl.ev[2], s));
     launch_pyramid(dframes, fstride, dpitch, w, h, ctx->arena.as<uint8_t>(), ctx->level_frame_stride,
                    ctx->d_levels.as<LevelInfo>(), ctx->levels.data(), L, ctx->d_tabs.as<uint32_t>(), n, s);
-    if (timing) CU(cudaEventRecord(ctx->ev[2], s));
+    CU(cudaEventRecord(sl.ev[3], s));
     launch_stage1(ctx->w1, ctx->T1, ctx->arena.as<uint8_t>(), ctx->level_frame_stride,
                   ctx->d_levels.as<LevelInfo>(), ctx->d_tasks.as<S1Task>(),
                   ctx->d_cta_first.as<int32_t>(), (int)ctx->cta_first.size() - 1,
-                  ctx->cands.as<S1Cand>(), cand_cap, ctx->ctrl.as<Ctrl>(),
+                  ctx->cands.as<S1Cand>(), cand_cap, dctrl,
                   dbg1 ? ctx->dbg_map.as<float>() : nullptr, ctx->map_frame_stride, s);
-    if (timing) CU(cudaEventRecord(ctx->ev[3], s));
+    CU(cudaEventRecord(sl.ev[4], s));
     launch_selective(ctx->w2, ctx->w3, ctx->sp, dframes, fstride, dpitch, w, h,
                      ctx->d_levels.as<LevelInfo>(), ctx->cands.as<S1Cand>(), cand_cap,
                      ctx->selout.as<SelOut>(), dbg1 ? ctx->dbg_resp.as<float>() : nullptr,
-                     ctx->acc.as<AccBox>(), ctx->ctrl.as<Ctrl>(), ctx->sm_count, s);
-    if (timing) CU(cudaEventRecord(ctx->ev[4], s));
-    launch_nms(ctx->acc.as<AccBox>(), ctx->ctrl.as<Ctrl>(), n, ctx->min_cluster,
-               ctx->staging.as<OutBox>(), ctx->counts.as<int32_t>(), ctx->out.as<OutBox>(), s);
+                     ctx->acc.as<AccBox>(), dctrl, ctx->sm_count, s);
+    CU(cudaEventRecord(sl.ev[5], s));
+    launch_nms(ctx->acc.as<AccBox>(), dctrl, n, ctx->min_cluster, ctx->staging.as<OutBox>(),
+               ctx->counts.as<int32_t>(), sl.out.as<OutBox>(), s);
     CU(cudaGetLastError());
-    CU(cudaMemcpyAsync(ctx->h_ctrl, ctx->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
-    if (timing) CU(cudaEventRecord(ctx->ev[5], s));
-    CU(cudaStreamSynchronize(s));
-    const Ctrl& hc = *ctx->h_ctrl;
+    CU(cudaMemcpyAsync(sl.h_ctrl, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    CU(cudaEventRecord(sl.ev[6], s));
+    sl.used = true;
+    ctx->next_slot ^= 1;
+    ctx->inflight++;
+    return CCNN_OK;
+}
+
+int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes, ccnn_stats* stats)
+{
+    if (!ctx) return CCNN_E_ARG;
+    if (!n_boxes || (box_cap > 0 && !boxes)) return fail(ctx, CCNN_E_ARG, "NULL n_boxes / boxes");
+    if (ctx->inflight == 0) return fail(ctx, CCNN_E_STATE, "no batch in flight");
+    CU(cudaSetDevice(ctx->device));
+    const int si = ctx->next_slot ^ (ctx->inflight == 2 ? 0 : 1);     // oldest in-flight slot
+    ccnn_ctx::Slot& sl = ctx->slot[si];
+    ctx->inflight--;
+    ctx->last_slot = si;
+    ctx->last_valid = false;
+    CU(cudaEventSynchronize(sl.ev[6]));
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->windows = sl.windows;
+    }
+    ctx->last_n = sl.n;
+    if (sl.empty) {
+        *n_boxes = 0;
+        ctx->last_cands = 0;
+        ctx->last_nout = 0;
+        ctx->last_valid = true;
+        return CCNN_OK;
+    }
+    const Ctrl& hc = *sl.h_ctrl;
     ctx->last_cands = hc.n_cand;
-    if (hc.n_cand > cand_cap)
+    if (hc.n_cand > sl.cand_cap)
         return fail(ctx, CCNN_E_QUEUE, "stage-1 survivor queue overflow: " + std::to_string(hc.n_cand) +
-                                           " > capacity " + std::to_string(cand_cap));
+                                           " > capacity " + std::to_string(sl.cand_cap));
     if (hc.nms_overflow)
         return fail(ctx, CCNN_E_QUEUE, "more than 4096 accepted regions in one frame");
     ctx->last_valid = true;
@@ -498,9 +563,10 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
         stats->stage3 = hc.n_stage3;
         stats->nms = hc.n_out;
         stats->kernel_launches = 4;
-        float t;
+        const int from[5] = {0, 2, 3, 4, 5}, to[5] = {1, 3, 4, 5, 6};
         for (int k = 0; k < 5; ++k) {
-            cudaEventElapsedTime(&t, ctx->ev[k], ctx->ev[k + 1]);
+            float t = 0.f;
+            cudaEventElapsedTime(&t, sl.ev[from[k]], sl.ev[to[k]]);
             stats->ms[k] = t;
         }
     }
@@ -510,10 +576,24 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
         return fail(ctx, CCNN_E_CAPACITY, "box_cap too small: need " + std::to_string(hc.n_out));
     if (hc.n_out) {
         static_assert(sizeof(OutBox) == sizeof(ccnn_box), "OutBox mirrors ccnn_box");
-        CU(cudaMemcpyAsync(boxes, ctx->out.p, sizeof(OutBox) * hc.n_out, cudaMemcpyDeviceToHost, s));
-        CU(cudaStreamSynchronize(s));
+        CU(cudaMemcpyAsync(boxes, sl.out.p, sizeof(OutBox) * hc.n_out, cudaMemcpyDeviceToHost,
+                           ctx->d2h_stream));
+        CU(cudaStreamSynchronize(ctx->d2h_stream));
     }
     return CCNN_OK;
+}
+
+int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64_t pitch,
+                int frames_on_device, int min_face, float scale_step, ccnn_box* boxes,
+                int64_t box_cap, int64_t* n_boxes, ccnn_stats* stats)
+{
+    if (!ctx) return CCNN_E_ARG;
+    if (!n_boxes || (box_cap > 0 && !boxes)) return fail(ctx, CCNN_E_ARG, "NULL n_boxes / boxes");
+    if (ctx->inflight) return fail(ctx, CCNN_E_STATE, "ccnn_detect with batches in flight");
+    const int rc = ccnn_submit(ctx, frames, n, w, h, pitch, frames_on_device, min_face, scale_step,
+                               stats != nullptr);
+    if (rc != CCNN_OK) return rc;
+    return ccnn_collect(ctx, boxes, box_cap, n_boxes, stats);
 }
 
 int ccnn_last_boxes(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes)
@@ -525,9 +605,9 @@ int ccnn_last_boxes(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_
         return fail(ctx, CCNN_E_CAPACITY, "box_cap too small: need " + std::to_string(ctx->last_nout));
     if (ctx->last_nout) {
         CU(cudaSetDevice(ctx->device));
-        CU(cudaMemcpyAsync(boxes, ctx->out.p, sizeof(OutBox) * ctx->last_nout, cudaMemcpyDeviceToHost,
-                           ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
+        CU(cudaMemcpyAsync(boxes, ctx->slot[ctx->last_slot].out.p, sizeof(OutBox) * ctx->last_nout,
+                           cudaMemcpyDeviceToHost, ctx->d2h_stream));
+        CU(cudaStreamSynchronize(ctx->d2h_stream));
     }
     return CCNN_OK;
 }
@@ -579,8 +659,9 @@ int ccnn_debug_stage1_map(ccnn_ctx* ctx, int frame, int level, float* out, int64
 int ccnn_debug_counters(ccnn_ctx* ctx, uint32_t* out, int cap)
 {
     if (!ctx || !out) return CCNN_E_ARG;
-    const int n = (int)(sizeof(ctx->h_ctrl->pad) / sizeof(uint32_t));
-    for (int k = 0; k < n && k < cap; ++k) out[k] = ctx->h_ctrl->pad[k];
+    const Ctrl* hc = ctx->slot[ctx->last_slot].h_ctrl;
+    const int n = (int)(sizeof(hc->pad) / sizeof(uint32_t));
+    for (int k = 0; k < n && k < cap; ++k) out[k] = hc->pad[k];
     return n;
 }
 

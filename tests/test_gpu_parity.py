@@ -220,3 +220,34 @@ def test_host_vs_device_frames_and_determinism(ws):
     big[:, :, :c.width] = dev
     f = det.detect(big[:, :, :c.width], c.min_face, c.scale_step)
     assert np.array_equal(a, f)
+
+
+def test_streaming_submit_collect(ws):
+    """ccnn_submit / ccnn_collect (two batches in flight, H2D overlapped) returns exactly what
+    ccnn_detect returns, in submission order; the in-flight limit and detect-while-in-flight
+    are errors."""
+    import torch
+    from paper_1508_01292_b200 import ccnn
+    c = configs.C3
+    T1, T2 = c.thresholds()
+    batches = [c.make_frames(3, seed=configs.FRAME_SEED + 11 * k) for k in range(4)]
+    det = make_det(ws, T1, T2, c.Tnn, c.rule, max_batch=4)
+    ref = [det.detect(b, c.min_face, c.scale_step) for b in batches]
+    pinned = [torch.from_numpy(b).pin_memory() for b in batches]
+    got = []
+    for k, b in enumerate(pinned):
+        det.submit(b, c.min_face, c.scale_step)
+        if k:
+            got.append(det.collect())
+    with pytest.raises(ccnn.CcnnError) as e:         # one in flight: detect is refused
+        det.detect(batches[0], c.min_face, c.scale_step)
+    assert e.value.code == ccnn.CCNN_E_STATE
+    det.submit(pinned[0], c.min_face, c.scale_step)
+    with pytest.raises(ccnn.CcnnError) as e:         # a third batch is refused
+        det.submit(pinned[1], c.min_face, c.scale_step)
+    assert e.value.code == ccnn.CCNN_E_STATE
+    got.append(det.collect())
+    got.append(det.collect())
+    for k in range(4):
+        assert np.array_equal(got[k], ref[k])
+    assert np.array_equal(got[4], ref[0])
