@@ -48,11 +48,20 @@ struct LevelInfo {             // one pyramid level (same for every frame of a b
     int32_t tab_off;           // offset of the level's x table (lw entries) then y table (lh)
     int32_t row0;              // rows of all earlier levels (pyramid grid: one CTA per level row)
 };
-struct S1Task {                // one stage-1 CTA task: a band of windows on one level
+// One stage-1 CTA task: a band of TW = 59 window columns x a segment of rows.  Patchwork
+// (SURVEY §8(f) NEXT #1): a band holds up to kMaxPieces pieces of levels
+// side by side -- piece p = window columns [x0, x0+w) of `level`, placed at band window
+// column J; consecutive pieces are kPieceGap windows apart so no valid window straddles
+// two pieces (the windows in the gap are computed and discarded).
+constexpr int kMaxPieces = 4;
+constexpr int kPieceGap = 6;       // 4*6 = 24 > 23 = input columns a window reaches past 4j
+struct S1Piece { int16_t level, x0, w, J; };
+struct S1Task {
     int32_t frame;
-    int16_t level, bw;         // level, band width in windows (<= TW)
-    int16_t x0, y0;            // first window column / row
-    int16_t nrows, pad;        // window rows in this task
+    int16_t y0, nrows;             // first window row / window rows (shared by all pieces)
+    int16_t npieces, pad0;
+    int32_t pad1;
+    S1Piece piece[kMaxPieces];
 };
 struct S1Cand {                // stage-1 survivor record (16 B)
     int32_t frame;

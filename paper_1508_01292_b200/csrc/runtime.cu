@@ -249,22 +249,63 @@ void build_plan(ccnn_ctx* c, int n, int W, int H, int min_face, float scale_step
     // segment height: the tallest segments (least vertical halo recompute) whose largest
     // task still fits in half the average load of a CTA slot, so the dynamic list schedule
     // balances (ccnn_params.segment_rows > 0 forces a height)
+    // bands: every full TW-wide band of a level is its own band; the tail pieces (the last,
+    // narrower band of each level, or a whole narrow level) are packed side by side into
+    // shared bands, first-fit by decreasing height (patchwork)
+    struct Band { int npieces; S1Piece piece[kMaxPieces]; int height; int used; };
+    std::vector<Band> bands;
+    std::vector<S1Piece> tails;
+    for (int l = 0; l < (int)c->levels.size(); ++l) {
+        const LevelInfo& L = c->levels[l];
+        int x0 = 0;
+        for (; x0 + TW <= L.nx; x0 += TW) {
+            Band b{};
+            b.npieces = 1;
+            b.piece[0] = S1Piece{(int16_t)l, (int16_t)x0, (int16_t)TW, 0};
+            b.height = L.ny;
+            b.used = TW;
+            bands.push_back(b);
+        }
+        if (x0 < L.nx) tails.push_back(S1Piece{(int16_t)l, (int16_t)x0, (int16_t)(L.nx - x0), 0});
+    }
+    std::stable_sort(tails.begin(), tails.end(), [&](const S1Piece& a, const S1Piece& b) {
+        return c->levels[a.level].ny > c->levels[b.level].ny;
+    });
+    const size_t first_tail_band = bands.size();
+    for (const S1Piece& t : tails) {
+        bool placed = false;
+        for (size_t k = first_tail_band; k < bands.size() && !placed; ++k) {
+            Band& b = bands[k];
+            if (b.npieces < kMaxPieces && b.used + kPieceGap + t.w <= TW) {
+                S1Piece p = t;
+                p.J = (int16_t)(b.used + kPieceGap);
+                b.piece[b.npieces++] = p;
+                b.used = p.J + p.w;
+                placed = true;
+            }
+        }
+        if (!placed) {
+            Band b{};
+            b.npieces = 1;
+            b.piece[0] = t;
+            b.height = c->levels[t.level].ny;   // tallest first: the band's height
+            b.used = t.w;
+            bands.push_back(b);
+        }
+    }
     auto make_tasks = [&](int seg, std::vector<S1Task>& one) {
         one.clear();
-        for (int l = 0; l < (int)c->levels.size(); ++l) {
-            const LevelInfo& L = c->levels[l];
-            const int nseg = std::max(1, (L.ny + seg - 1) / seg);
-            const int rows = (L.ny + nseg - 1) / nseg;
-            for (int x0 = 0; x0 < L.nx; x0 += TW)
-                for (int y0 = 0; y0 < L.ny; y0 += rows) {
-                    S1Task t{};
-                    t.level = (int16_t)l;
-                    t.bw = (int16_t)std::min(TW, L.nx - x0);
-                    t.x0 = (int16_t)x0;
-                    t.y0 = (int16_t)y0;
-                    t.nrows = (int16_t)std::min(rows, L.ny - y0);
-                    one.push_back(t);
-                }
+        for (const Band& b : bands) {
+            const int nseg = std::max(1, (b.height + seg - 1) / seg);
+            const int rows = (b.height + nseg - 1) / nseg;
+            for (int y0 = 0; y0 < b.height; y0 += rows) {
+                S1Task t{};
+                t.y0 = (int16_t)y0;
+                t.nrows = (int16_t)std::min(rows, b.height - y0);
+                t.npieces = (int16_t)b.npieces;
+                for (int p = 0; p < b.npieces; ++p) t.piece[p] = b.piece[p];
+                one.push_back(t);
+            }
         }
     };
     std::vector<S1Task> one;

@@ -60,8 +60,11 @@ constexpr int P1_RING = 6;              // rows 4v-2 .. 4v+3
 constexpr int P2_RS = NT / 2 + 8;
 constexpr int P2_RING = 4;              // rows 2v-3 .. 2v
 constexpr int SMEM_FLOATS = IN_RING * IN_RS + P1_RING * 6 * P1_RS + P2_RING * 6 * P2_RS;
-constexpr int LOAD_WORDS = 8 * IN_WORDS;                 // 8 new input rows per super-step
-constexpr int LOAD_SLOTS = (LOAD_WORDS + NT - 1) / NT;
+// loader: 8 new input rows x 65 words per super-step = 520 loads on 128 threads.  Thread t
+// owns ONE word column (t < 65: word t of rows 0-3; else word t-65 of rows 4-7) plus, for
+// t < 8, one leftover (word 63 + (t&1) of row 4 + (t>>1)) -- so a thread's loads come from
+// at most two source columns and its source descriptors stay in registers.
+static_assert(IN_WORDS == 65 && NT == 128, "loader mapping");
 
 __device__ __forceinline__ float u8f(uint32_t v)
 {
@@ -102,15 +105,10 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
     const int j3 = 16 * warp + (lane >> 1);
     const int r3 = lane & 1;
 
-    int ld_row[LOAD_SLOTS], ld_w[LOAD_SLOTS];
-    bool ld_ok[LOAD_SLOTS];
-#pragma unroll
-    for (int k = 0; k < LOAD_SLOTS; ++k) {
-        const int g = tid + k * NT;
-        ld_ok[k] = g < LOAD_WORDS;
-        ld_row[k] = g / IN_WORDS;
-        ld_w[k] = g % IN_WORDS;
-    }
+    const int ld_w = tid < IN_WORDS ? tid : tid - IN_WORDS;      // primary word column
+    const int ld_r0 = tid < IN_WORDS ? 0 : 4;                      // its rows ld_r0 .. +3
+    const bool ld_x = tid < 8;                                     // leftover load
+    const int ld_xw = 63 + (tid & 1), ld_xr = 4 + (tid >> 1);
 
     __shared__ int s_task;
     const int n_tasks = cta_first[gridDim.x];
@@ -120,24 +118,50 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
         const int ti = s_task;
         if (ti >= n_tasks) break;
         const S1Task T = tasks[ti];
-        const LevelInfo L = lvinfo[T.level];
         const int nrows = T.nrows;
-        const uint8_t* const band = levels + (int64_t)T.frame * level_frame_stride + L.offset +
-                                    (int64_t)(4 * T.x0);
         const int row_base = 4 * T.y0;
-        const int wmax = (L.pitch - 4 * T.x0) / 4 - 1;
-        auto gword = [&](int r, int w) -> uint32_t {
-            const int lr = min(row_base + r, L.lh - 1);
-            const int ww = min(w, wmax);
-            return __ldg(reinterpret_cast<const uint32_t*>(band + (int64_t)lr * L.pitch) + ww);
+        // piece of a band window column j: the last piece starting at or before j (patchwork);
+        // selected with predicated moves (no dynamic indexing -> no local memory)
+        auto piece_of = [&](int j) -> S1Piece {
+            S1Piece P = T.piece[0];
+#pragma unroll
+            for (int q = 1; q < kMaxPieces; ++q)
+                if (q < T.npieces && T.piece[q].J <= j) P = T.piece[q];
+            return P;
         };
+        // input word w of the band (columns 4w .. 4w+3) of band row r: the piece's level,
+        // clamped to its rows and its row pitch (gap columns read a neighbour: discarded)
+        // (32-bit word offset from `levels`, pitch in words | rows << 16): two registers
+        struct Src { uint32_t woff, pitch_lh; };
+        auto src_of = [&](int w) -> Src {
+            const S1Piece P = piece_of(w);
+            const LevelInfo& L = lvinfo[P.level];
+            const int lw = min(P.x0 + w - P.J, L.pitch / 4 - 1);
+            const int64_t off = ((int64_t)T.frame * level_frame_stride + L.offset) / 4 + lw;
+            return Src{(uint32_t)off, (uint32_t)(L.pitch / 4) | ((uint32_t)L.lh << 16)};
+        };
+        auto gword = [&](const Src& sc, int r) -> uint32_t {
+            const int row = min(row_base + r, (int)(sc.pitch_lh >> 16) - 1);
+            return __ldg(reinterpret_cast<const uint32_t*>(levels) + sc.woff +
+                         (uint32_t)row * (sc.pitch_lh & 0xFFFFu));
+        };
+        const Src lsrc = src_of(ld_w);
+        const Src xsrc = src_of(ld_x ? ld_xw : 0);
+        // the window column this thread emits (layer 3): its piece, level coordinates
+        const S1Piece PE = piece_of(j3);
+        const int e_level = PE.level;
+        const int e_x = PE.x0 + j3 - PE.J;
+        const bool e_col = (j3 >= PE.J) && (j3 < PE.J + PE.w);
+        const LevelInfo& LE = lvinfo[e_level];
+        const int e_rows = min(nrows, LE.ny - T.y0);       // rows of this piece in the segment
 
         // prologue: input rows 0..10 to the ring, rows 11..18 into registers
         for (int g = tid; g < 11 * IN_WORDS; g += NT)
-            store_word(in_ring, g / IN_WORDS, g % IN_WORDS, gword(g / IN_WORDS, g % IN_WORDS));
-        uint32_t pre[LOAD_SLOTS];
+            store_word(in_ring, g / IN_WORDS, g % IN_WORDS, gword(src_of(g % IN_WORDS), g / IN_WORDS));
+        uint32_t pre[4], prex;
 #pragma unroll
-        for (int k = 0; k < LOAD_SLOTS; ++k) pre[k] = ld_ok[k] ? gword(11 + ld_row[k], ld_w[k]) : 0u;
+        for (int k = 0; k < 4; ++k) pre[k] = gword(lsrc, 11 + ld_r0 + k);
+        prex = ld_x ? gword(xsrc, 11 + ld_xr) : 0u;
 
         float acc3[2][6], carry[2] = {0.f, 0.f};
 #pragma unroll
@@ -197,11 +221,12 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
             // ---- loader: input rows 8v+11 .. 8v+18 into the slots of 8v .. 8v+7 (fetched
             //      during the previous super-step), then prefetch rows 8v+19 .. 8v+26 ----
 #pragma unroll
-            for (int k = 0; k < LOAD_SLOTS; ++k)
-                if (ld_ok[k]) store_word(in_ring, (8 * v + 11 + ld_row[k]) % IN_RING, ld_w[k], pre[k]);
+            for (int k = 0; k < 4; ++k)
+                store_word(in_ring, (8 * v + 11 + ld_r0 + k) % IN_RING, ld_w, pre[k]);
+            if (ld_x) store_word(in_ring, (8 * v + 11 + ld_xr) % IN_RING, ld_xw, prex);
 #pragma unroll
-            for (int k = 0; k < LOAD_SLOTS; ++k)
-                pre[k] = ld_ok[k] ? gword(8 * v + 19 + ld_row[k], ld_w[k]) : 0u;
+            for (int k = 0; k < 4; ++k) pre[k] = gword(lsrc, 8 * v + 19 + ld_r0 + k);
+            if (ld_x) prex = gword(xsrc, 8 * v + 19 + ld_xr);
 
             // ---- L2: conv3x3 6->6, pool, act -> P2 row p = 2v-1+r2 (P1 rows 2p .. 2p+3) ----
             {
@@ -294,10 +319,10 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
                 const float a0 = act(fin[0] + W.b3[0]);
                 const float a1 = act(fin[1] + W.b3[1]);
                 const float score = act(fmaf(W.w4[1], a1, fmaf(W.w4[0], a0, W.b4)));
-                const bool valid = (o >= 0) && (o < nrows) && (j3 < T.bw);
+                const bool valid = (o >= 0) && (o < e_rows) && e_col;
                 if (DEBUG && valid)
-                    dbg_map[(int64_t)T.frame * dbg_map_frame_stride + L.map_off +
-                            (int64_t)(T.y0 + o) * L.nx + (T.x0 + j3)] = score;
+                    dbg_map[(int64_t)T.frame * dbg_map_frame_stride + LE.map_off +
+                            (int64_t)(T.y0 + o) * LE.nx + e_x] = score;
                 const bool pred = valid && (score > T1);             // "exceeded"
                 const unsigned mask = __ballot_sync(0xFFFFFFFFu, pred);
                 if (mask) {
@@ -310,9 +335,9 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
                         if (idx < cand_cap) {
                             S1Cand cd;
                             cd.frame = T.frame;
-                            cd.level = T.level;
+                            cd.level = (int16_t)e_level;
                             cd.pad = 0;
-                            cd.ix = (int16_t)(T.x0 + j3);
+                            cd.ix = (int16_t)e_x;
                             cd.iy = (int16_t)(T.y0 + o);
                             cd.s1 = score;
                             cands[idx] = cd;
