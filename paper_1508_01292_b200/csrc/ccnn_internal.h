@@ -46,8 +46,10 @@ struct LevelInfo {             // one pyramid level (same for every frame of a b
     int32_t nx, ny;            // window grid
     int32_t map_off;           // offset of the level in one frame's dense stage-1 map (debug)
     int32_t tab_off;           // offset of the level's x table (lw entries) then y table (lh)
-    int32_t row0;              // rows of all earlier levels (pyramid grid: one CTA per level row)
+    int32_t row0;              // rows of all earlier levels
+    int32_t cta0;              // pyramid tiles (128 columns x kPyrRows rows) of all earlier levels
 };
+constexpr int kPyrCols = 128, kPyrRows = 8;   // pyramid CTA tile
 // One stage-1 CTA task: a band of TW = 59 window columns x a segment of rows.  Patchwork
 // (SURVEY §8(f) NEXT #1): a band holds up to kMaxPieces pieces of levels
 // side by side -- piece p = window columns [x0, x0+w) of `level`, placed at band window

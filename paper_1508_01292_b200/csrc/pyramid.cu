@@ -9,66 +9,66 @@
 // integer arithmetic.
 //
 // Roofline: HBM-bound in principle (the frame read once + 1 B written per level pixel;
-// DESIGN.md "Roofline"), in practice issue/ALU-bound on the byte gathers.  One CTA per
-// (level row, frame) does the row setup once; its lanes stride over CONSECUTIVE output
-// pixels, so each warp's byte gathers from the frame stay within 32/sigma bytes and its
-// byte stores form one 32-byte sector; 4 pixels per lane are in flight at once.
-// Measured alternatives: 4 adjacent pixels per lane spread every
-// load instruction 4x wider; staging whole source rows in shared memory moved 5x the
-// frame through L2; one pixel per thread with a flat grid paid the row setup per pixel.
+// DESIGN.md "Roofline"), in practice issue-bound on the byte gathers.  A CTA owns a tile
+// of 128 consecutive output columns x 8 rows of one level: each thread loads its column's
+// x-table entry once and walks the rows; the row setup is CTA-uniform; adjacent lanes
+// gather adjacent output pixels (their frame reads stay within 32/sigma bytes) and store
+// one 128-byte line per warp-row; all 8 rows' gathers are issued before any blend.
+// Measured alternatives: 4 adjacent pixels per lane, whole source
+// rows staged in shared memory, one pixel per thread on a flat grid, CTA per output row.
 #include "ccnn_internal.h"
 
 namespace ccnn {
 namespace {
 
-constexpr int kPyrThreads = 128;
-
 template <bool SAFE>
-__global__ void __launch_bounds__(kPyrThreads) pyramid_kernel(
+__global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
     const uint8_t* __restrict__ frames, int64_t frame_stride, int64_t pitch, int W, int H,
     uint8_t* __restrict__ levels, int64_t level_frame_stride,
     const LevelInfo* __restrict__ lv, int n_levels, const uint32_t* __restrict__ tabs)
 {
-    const int row = blockIdx.x;                        // row of the concatenated levels
     const int f = blockIdx.y;
     int l = 0;
-    while (l + 1 < n_levels && lv[l + 1].row0 <= row) ++l;
+    while (l + 1 < n_levels && lv[l + 1].cta0 <= (int)blockIdx.x) ++l;
     const LevelInfo& L = lv[l];
-    const int y = row - L.row0;
-    const uint32_t yt = __ldg(tabs + L.tab_off + L.lw + y);
+    const int tiles_x = (L.pitch + kPyrCols - 1) / kPyrCols;
+    const int t = blockIdx.x - L.cta0;
+    const int ty = t / tiles_x, tx = t - ty * tiles_x;
+    const int xo = tx * kPyrCols + threadIdx.x;                // output column (pitch-padded)
+    if (xo >= L.pitch) return;
     // SAFE (W, H >= 2): the tables encode the edge so that i1 = i0 + 1 always (runtime.cu
     // sample_entry); otherwise the clamped form
-    const uint32_t y0 = yt & 0xFFFFu, ay = yt >> 16;
-    const uint32_t y1 = SAFE ? y0 + 1u : min(y0 + 1u, (uint32_t)(H - 1));
+    const uint32_t e = __ldg(tabs + L.tab_off + min(xo, L.lw - 1));   // padding = edge pixel
+    const uint32_t x0 = e & 0xFFFFu;
+    const uint32_t x1 = SAFE ? x0 + 1u : min(x0 + 1u, (uint32_t)(W - 1));
+    const int ax = (int)(e >> 16);
     const uint8_t* src = frames + (int64_t)f * frame_stride;
-    const uint8_t* __restrict__ r0 = src + (int64_t)y0 * pitch;
-    const uint8_t* __restrict__ r1 = src + (int64_t)y1 * pitch;
-    const uint32_t* __restrict__ xt = tabs + L.tab_off;
-    uint8_t* dst = levels + (int64_t)f * level_frame_stride + L.offset + (int64_t)y * L.pitch;
-    const int lwm = L.lw - 1;
-    for (int xb = threadIdx.x; xb < L.pitch; xb += 4 * kPyrThreads) {
-        uint32_t e[4];
+    uint8_t* dst = levels + (int64_t)f * level_frame_stride + L.offset + xo;
+    const uint32_t* yt = tabs + L.tab_off + L.lw;
+    const int y_beg = ty * kPyrRows;
+    const int nr = min(kPyrRows, L.lh - y_beg);                 // CTA-uniform
+    // all rows' table entries and frame bytes are loaded before any blend: 8 rows of
+    // independent gathers in flight per thread
+    int p[kPyrRows][4], ay[kPyrRows];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) e[u] = __ldg(xt + min(xb + u * kPyrThreads, lwm));
-        int p[4][4];
+    for (int r = 0; r < kPyrRows; ++r) {
+        const uint32_t ye = __ldg(yt + y_beg + min(r, nr - 1));
+        const uint32_t y0 = ye & 0xFFFFu;
+        const uint32_t y1 = SAFE ? y0 + 1u : min(y0 + 1u, (uint32_t)(H - 1));
+        ay[r] = (int)(ye >> 16);
+        const uint8_t* r0 = src + (int64_t)y0 * pitch;
+        const uint8_t* r1 = src + (int64_t)y1 * pitch;
+        p[r][0] = __ldg(r0 + x0);
+        p[r][1] = __ldg(r0 + x1);
+        p[r][2] = __ldg(r1 + x0);
+        p[r][3] = __ldg(r1 + x1);
+    }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t x0 = e[u] & 0xFFFFu;
-            p[u][0] = __ldg(r0 + x0);
-            p[u][1] = SAFE ? __ldg(r0 + x0 + 1) : __ldg(r0 + min(x0 + 1u, (uint32_t)(W - 1)));
-            p[u][2] = __ldg(r1 + x0);
-            p[u][3] = SAFE ? __ldg(r1 + x0 + 1) : __ldg(r1 + min(x0 + 1u, (uint32_t)(W - 1)));
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int xo = xb + u * kPyrThreads;
-            const int ax = (int)(e[u] >> 16);
-            // p0*(2048-a) + p1*a == (p0 << 11) + (p1 - p0)*a, exactly (O2)
-            const int top = (p[u][0] << 11) + (p[u][1] - p[u][0]) * ax;
-            const int bot = (p[u][2] << 11) + (p[u][3] - p[u][2]) * ax;
-            const int v = ((top << 11) + (bot - top) * (int)ay + (1 << 21)) >> 22;
-            if (xo < L.pitch) dst[xo] = (uint8_t)v;      // pitch padding replicates the edge
-        }
+    for (int r = 0; r < kPyrRows; ++r) {
+        // p0*(2048-a) + p1*a == (p0 << 11) + (p1 - p0)*a, exactly (O2)
+        const int top = (p[r][0] << 11) + (p[r][1] - p[r][0]) * ax;
+        const int bot = (p[r][2] << 11) + (p[r][3] - p[r][2]) * ax;
+        if (r < nr) dst[(int64_t)(y_beg + r) * L.pitch] = (uint8_t)(((top << 11) + (bot - top) * ay[r] + (1 << 21)) >> 22);
     }
 }
 
@@ -81,13 +81,14 @@ void launch_pyramid(const uint8_t* frames, int64_t frame_stride, int64_t pitch, 
 {
     if (n_levels <= 0) return;
     const LevelInfo& last = h_levels[n_levels - 1];
-    dim3 grid(last.row0 + last.lh, n);
+    const int tiles = last.cta0 + ((last.pitch + kPyrCols - 1) / kPyrCols) * ((last.lh + kPyrRows - 1) / kPyrRows);
+    dim3 grid(tiles, n);
     if (W >= 2 && H >= 2)
-        pyramid_kernel<true><<<grid, kPyrThreads, 0, s>>>(frames, frame_stride, pitch, W, H, levels,
-                                                          level_frame_stride, d_levels, n_levels, d_tabs);
+        pyramid_kernel<true><<<grid, kPyrCols, 0, s>>>(frames, frame_stride, pitch, W, H, levels,
+                                                       level_frame_stride, d_levels, n_levels, d_tabs);
     else
-        pyramid_kernel<false><<<grid, kPyrThreads, 0, s>>>(frames, frame_stride, pitch, W, H, levels,
-                                                           level_frame_stride, d_levels, n_levels, d_tabs);
+        pyramid_kernel<false><<<grid, kPyrCols, 0, s>>>(frames, frame_stride, pitch, W, H, levels,
+                                                        level_frame_stride, d_levels, n_levels, d_tabs);
 }
 
 }  // namespace ccnn

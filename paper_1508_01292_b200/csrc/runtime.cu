@@ -216,7 +216,7 @@ void build_plan(ccnn_ctx* c, int n, int W, int H, int min_face, float scale_step
     const double sf = (double)scale_step;
     double s = (double)kWinW / (double)min_face;
     int64_t off = 0, map_off = 0;
-    int64_t row0 = 0;
+    int64_t row0 = 0, cta0 = 0;
     c->windows_per_frame = 0;
     while (true) {
         const int lw = (int)std::floor((double)W * s);
@@ -233,6 +233,8 @@ void build_plan(ccnn_ctx* c, int n, int W, int H, int min_face, float scale_step
         L.map_off = (int32_t)map_off;
         L.tab_off = (int32_t)c->tabs.size();
         L.row0 = (int32_t)row0;                      // rows of earlier levels
+        L.cta0 = (int32_t)cta0;                      // pyramid tiles of earlier levels
+        cta0 += (int64_t)((L.pitch + kPyrCols - 1) / kPyrCols) * ((lh + kPyrRows - 1) / kPyrRows);
         for (int x = 0; x < lw; ++x) c->tabs.push_back(sample_entry(x, s, W));
         for (int y = 0; y < lh; ++y) c->tabs.push_back(sample_entry(y, s, H));
         off += round_up((int64_t)L.pitch * lh, 256);
