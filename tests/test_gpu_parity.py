@@ -251,3 +251,17 @@ def test_streaming_submit_collect(ws):
     for k in range(4):
         assert np.array_equal(got[k], ref[k])
     assert np.array_equal(got[4], ref[0])
+
+
+@pytest.mark.parametrize("seg", [1, 3, 7])
+def test_segment_heights_and_patchwork(ws, cascade, seg):
+    """Forced short segments (every task boundary, priming and ring wrap-around) and
+    patchwork bands (many narrow levels of a 1080p frame packed side by side): the dense
+    stage-1 maps and survivors still match the oracle."""
+    c = configs.C3
+    fr = c.make_frames(1)
+    T1 = quantile_T1(cascade, fr, 96, 1.25, 0.999)
+    det = make_det(ws, T1, (0.9, 0.2), 2, 0, max_batch=2, segment_rows=seg)
+    rep = parity.compare_run(det, cascade, fr, 96, 1.25, T1, (0.9, 0.2), 2, 0, check_levels=False)
+    assert rep["survivors"] > 10
+    print(rep)
