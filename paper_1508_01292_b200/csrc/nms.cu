@@ -53,12 +53,13 @@ __device__ __forceinline__ bool iou_edge(short4 a, short4 b)
 // parents strictly decreases the index; path halving (parent[k] = grandparent) keeps the
 // invariant, so concurrent halving writes are benign.  Without it, dense clutter graphs
 // built parent chains hundreds long (C5: 3.4 ms per 16 frames).
-__device__ __forceinline__ int find_root(volatile int* parent, int k)
+__device__ __forceinline__ int find_root(int* parent, int k)
 {
-    int p = parent[k];
+    volatile int* vp = parent;
+    int p = vp[k];
     while (p != k) {                 // path splitting: every visited node skips to its grandparent
-        const int gp = parent[p];
-        parent[k] = gp;
+        const int gp = vp[p];
+        if (gp != p) atomicMin(&parent[k], gp);   // monotone (parent[x] <= x): benign, atomic
         k = p;
         p = gp;
     }

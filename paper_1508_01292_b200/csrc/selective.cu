@@ -191,8 +191,11 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
             }
         }
     } else {
-        for (int it = tid; it < C * 50; it += kSelThreads) {
-            const int m = it / 50, idx = it - m * 50;
+        // map-major items padded to 64 per map: every warp works on one map, so its weight
+        // loads are one broadcast address (no serialised constant-cache accesses)
+        for (int it = tid; it < C * 64; it += kSelThreads) {
+            const int m = it >> 6, idx = it & 63;
+            if (idx >= 50) continue;
             const int o = idx / 25, cell = idx - o * 25, y = cell / 5, x = cell - y * 5;
             float s = W.b3[m];
 #pragma unroll
@@ -258,19 +261,36 @@ __global__ void __launch_bounds__(kSelThreads, 2) selective_kernel(
         }
         if (tid < 256) sm.hist[tid] = 0;
         __syncthreads();
-        // ---- O2 fixed-point bilinear sampling from the ORIGINAL frame + histogram ----
-        for (int k = tid; k < kPatchN; k += kSelThreads) {
-            const int v = k / kPatchW, u = k - v * kPatchW;
-            const uint32_t xt = sm.colx[u], yt = sm.rowy[v];
-            const uint32_t x0 = xt & 0xFFFFu, ax = xt >> 16, y0 = yt & 0xFFFFu, ay = yt >> 16;
-            const uint32_t x1 = min(x0 + 1u, (uint32_t)(Wd - 1)), y1 = min(y0 + 1u, (uint32_t)(Hd - 1));
-            const uint8_t* r0 = frame + (int64_t)y0 * pitch;
-            const uint8_t* r1 = frame + (int64_t)y1 * pitch;
-            const uint32_t top = (uint32_t)__ldg(r0 + x0) * (2048u - ax) + (uint32_t)__ldg(r0 + x1) * ax;
-            const uint32_t bot = (uint32_t)__ldg(r1 + x0) * (2048u - ax) + (uint32_t)__ldg(r1 + x1) * ax;
-            const uint32_t val = (top * (2048u - ay) + bot * ay + (1u << 21)) >> 22;
-            sm.patch[k] = (uint8_t)val;
-            atomicAdd(&sm.hist[val], 1);
+        // ---- O2 fixed-point bilinear sampling from the ORIGINAL frame + histogram; 4 pixels
+        //      per thread per pass so their gathers are in flight together ----
+        for (int k0 = tid; k0 < kPatchN; k0 += 4 * kSelThreads) {
+            uint32_t px[4][4], axy[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = min(k0 + u * kSelThreads, kPatchN - 1);
+                const int v = k / kPatchW, uu = k - v * kPatchW;
+                const uint32_t xt = sm.colx[uu], yt = sm.rowy[v];
+                const uint32_t x0 = xt & 0xFFFFu, y0 = yt & 0xFFFFu;
+                const uint32_t x1 = min(x0 + 1u, (uint32_t)(Wd - 1)), y1 = min(y0 + 1u, (uint32_t)(Hd - 1));
+                const uint8_t* r0 = frame + (int64_t)y0 * pitch;
+                const uint8_t* r1 = frame + (int64_t)y1 * pitch;
+                px[u][0] = __ldg(r0 + x0);
+                px[u][1] = __ldg(r0 + x1);
+                px[u][2] = __ldg(r1 + x0);
+                px[u][3] = __ldg(r1 + x1);
+                axy[u] = (xt >> 16) | (yt & 0xFFFF0000u);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = k0 + u * kSelThreads;
+                if (k >= kPatchN) break;
+                const uint32_t ax = axy[u] & 0xFFFFu, ay = axy[u] >> 16;
+                const uint32_t top = px[u][0] * (2048u - ax) + px[u][1] * ax;
+                const uint32_t bot = px[u][2] * (2048u - ax) + px[u][3] * ax;
+                const uint32_t val = (top * (2048u - ay) + bot * ay + (1u << 21)) >> 22;
+                sm.patch[k] = (uint8_t)val;
+                atomicAdd(&sm.hist[val], 1);
+            }
         }
         __syncthreads();
         // ---- O6 histogram equalisation LUT (round half up), warp 0 ----
