@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define CCNN_ABI_VERSION 1
+#define CCNN_ABI_VERSION 2
 
 /* status codes */
 #define CCNN_OK          0
@@ -125,6 +125,24 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
                 int frames_on_device, int min_face, float scale_step,
                 ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes, ccnn_stats* stats);
 
+/* One frame of a variable-size batch (stills of mixed sizes, e.g.
+ * the FDDB benchmark images).  data: uint8 grayscale, w x h, row pitch `pitch`
+ * bytes (>= w); host or device memory per the call's frames_on_device. */
+typedef struct {
+    const uint8_t* data;
+    int32_t w, h;
+    int64_t pitch;
+} ccnn_frame;
+
+/* ccnn_detect over n frames of individual sizes: each frame gets its own level table
+ * (O1), all levels of all frames share one pyramid / stage-1 / selective / NMS launch.
+ * Every frame must satisfy 1 <= w <= max_w, 1 <= h <= max_h; box.frame indexes `frames`.
+ * Errors and ownership exactly as ccnn_detect.  ccnn_detect(frames, n, w, h, pitch) is
+ * this call with frames[f] = {frames + f*h*pitch, w, h, pitch}. */
+int ccnn_detect_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frames_on_device,
+                       int min_face, float scale_step,
+                       ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes, ccnn_stats* stats);
+
 /* Streaming form of ccnn_detect (a video stream).
  * ccnn_submit enqueues one batch (same arguments as ccnn_detect) and returns at once: host
  * frames are copied H2D on an internal copy stream into one of two per-ctx frame buffers,
@@ -140,6 +158,10 @@ int ccnn_submit(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
                 int frames_on_device, int min_face, float scale_step, int timed);
 int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes,
                  ccnn_stats* stats);
+/* Streaming form of ccnn_detect_frames (the ccnn_frame array itself may be reused at
+ * once; the pixel data it points to must stay valid until the batch is collected). */
+int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frames_on_device,
+                       int min_face, float scale_step, int timed);
 
 /* Copy the boxes of the last ccnn_detect / ccnn_collect on ctx (also valid after it
  * returned CCNN_E_CAPACITY, so a caller can fetch the result without detecting again;
@@ -163,8 +185,9 @@ int ccnn_abi_version(void);
 #define CCNN_DEBUG_STAGE1   2  /* also write every stage-1 response to a dense map */
 int ccnn_set_debug(ccnn_ctx* ctx, int flags);
 
-/* Level table of the last detect: up to cap levels, returns the level count (>= 0). */
-int ccnn_debug_levels(ccnn_ctx* ctx, double* sigma, int32_t* lw, int32_t* lh, int cap);
+/* Level table of frame `frame` of the last submitted batch: up to cap levels, returns
+ * that frame's level count (>= 0), or a negative status. */
+int ccnn_debug_levels(ccnn_ctx* ctx, int frame, double* sigma, int32_t* lw, int32_t* lh, int cap);
 
 /* Copy level `level` of frame `frame` (lw*lh bytes, row pitch lw) to host `out`. */
 int ccnn_debug_level(ccnn_ctx* ctx, int frame, int level, uint8_t* out, int64_t cap);

@@ -19,8 +19,8 @@ CCNN_E_CAPACITY, CCNN_E_QUEUE, CCNN_E_CUDA, CCNN_E_STATE = -4, -5, -6, -7
 CCNN_DEBUG_LEVELS, CCNN_DEBUG_STAGE1 = 1, 2
 
 # every entry point declared in include/ccnn.h
-EXPORTS = ("ccnn_create", "ccnn_set_stream", "ccnn_detect", "ccnn_submit", "ccnn_collect",
-           "ccnn_last_boxes", "ccnn_destroy", "ccnn_last_error",
+EXPORTS = ("ccnn_create", "ccnn_set_stream", "ccnn_detect", "ccnn_detect_frames",
+           "ccnn_submit", "ccnn_collect", "ccnn_submit_frames", "ccnn_last_boxes", "ccnn_destroy", "ccnn_last_error",
            "ccnn_abi_version", "ccnn_set_debug", "ccnn_debug_levels", "ccnn_debug_level",
            "ccnn_debug_stage1_map", "ccnn_debug_candidates", "ccnn_debug_counters")
 
@@ -51,6 +51,10 @@ class Params(C.Structure):
 class Box(C.Structure):
     _fields_ = [("frame", C.c_int32), ("x", C.c_int32), ("y", C.c_int32), ("w", C.c_int32),
                 ("h", C.c_int32), ("score", C.c_float), ("neighbors", C.c_int32)]
+
+
+class Frame(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("w", C.c_int32), ("h", C.c_int32), ("pitch", C.c_int64)]
 
 
 class Stats(C.Structure):
@@ -92,6 +96,10 @@ def load():
     L.ccnn_detect.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64,
                               C.c_int, C.c_int, C.c_float, _P(Box), C.c_int64, _P(C.c_int64),
                               _P(Stats)]
+    L.ccnn_detect_frames.argtypes = [C.c_void_p, _P(Frame), C.c_int, C.c_int, C.c_int, C.c_float,
+                                     _P(Box), C.c_int64, _P(C.c_int64), _P(Stats)]
+    L.ccnn_submit_frames.argtypes = [C.c_void_p, _P(Frame), C.c_int, C.c_int, C.c_int, C.c_float,
+                                     C.c_int]
     L.ccnn_last_boxes.argtypes = [C.c_void_p, _P(Box), C.c_int64, _P(C.c_int64)]
     L.ccnn_submit.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64,
                               C.c_int, C.c_int, C.c_float, C.c_int]
@@ -102,7 +110,7 @@ def load():
     L.ccnn_last_error.restype = C.c_char_p
     L.ccnn_abi_version.argtypes = []
     L.ccnn_set_debug.argtypes = [C.c_void_p, C.c_int]
-    L.ccnn_debug_levels.argtypes = [C.c_void_p, _P(C.c_double), _P(C.c_int32), _P(C.c_int32),
+    L.ccnn_debug_levels.argtypes = [C.c_void_p, C.c_int, _P(C.c_double), _P(C.c_int32), _P(C.c_int32),
                                     C.c_int]
     L.ccnn_debug_level.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_uint8), C.c_int64]
     L.ccnn_debug_stage1_map.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_float), C.c_int64]
@@ -214,6 +222,60 @@ class Detector:
                                   scale_step, 1 if timed else 0))
         self._inflight.append((keep, n))
 
+    def _frame_list(self, frames, stream):
+        """ccnn_frame array for a list of 2-D uint8 images (numpy arrays or torch tensors,
+        all on the host or all on the ctx device) of individual sizes."""
+        if len(frames) == 0:
+            raise ValueError("empty frame list")
+        keep, descs, dev = [], [], set()
+        for f in frames:
+            if hasattr(f, "data_ptr"):
+                import torch
+                assert f.dtype == torch.uint8 and f.dim() == 2 and f.stride(1) == 1
+                if f.is_cuda and stream is None:
+                    stream = torch.cuda.current_stream(f.device).cuda_stream
+                dev.add(bool(f.is_cuda))
+                keep.append(f)
+                descs.append(Frame(f.data_ptr(), f.shape[1], f.shape[0], f.stride(0)))
+            else:
+                a = np.asarray(f)
+                if a.dtype != np.uint8 or a.ndim != 2 or a.strides[1] != 1:
+                    a = np.ascontiguousarray(a, np.uint8)
+                dev.add(False)
+                keep.append(a)
+                descs.append(Frame(a.ctypes.data, a.shape[1], a.shape[0], a.strides[0]))
+        if len(dev) != 1:
+            raise ValueError("frames must be all on the host or all on the device")
+        arr = (Frame * len(descs))(*descs)
+        return arr, len(descs), 1 if dev.pop() else 0, keep, stream
+
+    def detect_frames(self, frames, min_face, scale_step, box_cap=None, stream=None):
+        """ccnn_detect_frames: a list of 2-D uint8 frames of individual sizes.  box.frame
+        indexes the list."""
+        L = load()
+        arr, n, on_device, keep, stream = self._frame_list(frames, stream)
+        if stream is not None:
+            self.set_stream(stream)
+        cap = box_cap if box_cap is not None else max(self._cap, 64 * n)
+        nb = C.c_int64()
+        st = Stats()
+        out = np.zeros(cap, BOX_DTYPE)
+        rc = L.ccnn_detect_frames(self.h, arr, n, on_device, min_face, scale_step,
+                                  out.ctypes.data_as(_P(Box)), cap, C.byref(nb), C.byref(st))
+        res = self._result(rc, nb, st, box_cap, out)
+        del keep
+        return res
+
+    def submit_frames(self, frames, min_face, scale_step, stream=None, timed=True):
+        """Enqueue a list of frames of individual sizes (ccnn_submit_frames)."""
+        L = load()
+        arr, n, on_device, keep, stream = self._frame_list(frames, stream)
+        if stream is not None:
+            self.set_stream(stream)
+        self._check(L.ccnn_submit_frames(self.h, arr, n, on_device, min_face, scale_step,
+                                         1 if timed else 0))
+        self._inflight.append((keep, n))
+
     def collect(self, box_cap=None):
         """Boxes of the oldest submitted batch (ccnn_collect)."""
         L = load()
@@ -227,25 +289,28 @@ class Detector:
         return self._result(rc, nb, st, box_cap, out)
 
     # ---- test hooks ----
-    def levels(self):
+    def levels(self, frame=0):
+        """(sigma, lw, lh) of every level of `frame` of the last submitted batch."""
         L = load()
-        n = L.ccnn_debug_levels(self.h, None, None, None, 0)
+        n = L.ccnn_debug_levels(self.h, frame, None, None, None, 0)
+        if n < 0:
+            self._check(n)
         sig = np.zeros(max(n, 1), np.float64)
         lw = np.zeros(max(n, 1), np.int32)
         lh = np.zeros(max(n, 1), np.int32)
-        L.ccnn_debug_levels(self.h, sig.ctypes.data_as(_P(C.c_double)),
+        L.ccnn_debug_levels(self.h, frame, sig.ctypes.data_as(_P(C.c_double)),
                             lw.ctypes.data_as(_P(C.c_int32)), lh.ctypes.data_as(_P(C.c_int32)), n)
         return [(float(sig[k]), int(lw[k]), int(lh[k])) for k in range(n)]
 
     def level_image(self, frame, level):
-        _, lw, lh = self.levels()[level]
+        _, lw, lh = self.levels(frame)[level]
         out = np.zeros((lh, lw), np.uint8)
         self._check(load().ccnn_debug_level(self.h, frame, level, out.ctypes.data_as(_P(C.c_uint8)),
                                             out.size))
         return out
 
     def stage1_map(self, frame, level):
-        _, lw, lh = self.levels()[level]
+        _, lw, lh = self.levels(frame)[level]
         nx, ny = (lw - 27) // 4 + 1, (lh - 31) // 4 + 1
         out = np.zeros((ny, nx), np.float32)
         self._check(load().ccnn_debug_stage1_map(self.h, frame, level,

@@ -39,27 +39,37 @@ using Cnn2W = SelNetW<16, 6, 2>;
 using Cnn3W = SelNetW<2, 2, 25>;
 
 // ---- per-call geometry ----
-struct LevelInfo {             // one pyramid level (same for every frame of a batch)
+struct FrameInfo {             // one frame of a batch, as the kernels read it
+    const uint8_t* data;       // device pointer
+    int64_t pitch;             // row pitch in bytes
+    int32_t w, h;
+    int32_t level0, nlevels;   // its levels: LevelInfo[level0 .. level0 + nlevels)
+    int32_t tiles, pad;        // pyramid tiles of all its levels
+};
+struct LevelInfo {             // one pyramid level of one frame of the batch
     double sigma;
-    int64_t offset;            // byte offset of the level inside one frame's level arena
+    int64_t offset;            // byte offset of the level in the level arena
+    int64_t map_off;           // offset of the level in the dense stage-1 map (debug)
     int32_t lw, lh, pitch;     // level size, row pitch (multiple of 16 B)
     int32_t nx, ny;            // window grid
-    int32_t map_off;           // offset of the level in one frame's dense stage-1 map (debug)
     int32_t tab_off;           // offset of the level's x table (lw entries) then y table (lh)
-    int32_t row0;              // rows of all earlier levels
-    int32_t cta0;              // pyramid tiles (128 columns x kPyrRows rows) of all earlier levels
+    int32_t frame;             // the frame this level belongs to
+    int32_t cta0;              // pyramid tiles (kPyrCols x kPyrRows) of the earlier levels of its frame
+    int32_t pad;
 };
 constexpr int kPyrCols = 128, kPyrRows = 8;   // pyramid CTA tile
+
 // One stage-1 CTA task: a band of TW = 59 window columns x a segment of rows.  Patchwork
 // (SURVEY §8(f) NEXT #1): a band holds up to kMaxPieces pieces of levels
-// side by side -- piece p = window columns [x0, x0+w) of `level`, placed at band window
+// side by side -- piece p = window columns [x0, x0+w) of `level` (a global level id: levels of
+// different frames may share a band), placed at band window
 // column J; consecutive pieces are kPieceGap windows apart so no valid window straddles
 // two pieces (the windows in the gap are computed and discarded).
 constexpr int kMaxPieces = 4;
 constexpr int kPieceGap = 6;       // 4*6 = 24 > 23 = input columns a window reaches past 4j
 struct S1Piece { int16_t level, x0, w, J; };
 struct S1Task {
-    int32_t frame;
+    int32_t frame;                 // frame of the first piece (informational)
     int16_t y0, nrows;             // first window row / window rows (shared by all pieces)
     int16_t npieces, pad0;
     int32_t pad1;
@@ -99,26 +109,23 @@ constexpr int kMaxLevels = 256;   // pyramid levels per frame (scale_step 1.02 s
 constexpr int kNmsCap = 4096;  // raw boxes per frame handled by one NMS CTA
 
 // ---- launchers (stream-ordered, no sync) ----
-// pyramid: every level of every frame from the original frames
-void launch_pyramid(const uint8_t* frames, int64_t frame_stride, int64_t pitch, int W, int H,
-                    uint8_t* levels, int64_t level_frame_stride, const LevelInfo* d_levels,
-                    const LevelInfo* h_levels, int n_levels, const uint32_t* d_tabs, int n,
+// pyramid: every level of every frame, from the original frames
+void launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, bool safe,
+                    uint8_t* levels, const LevelInfo* d_levels, const uint32_t* d_tabs,
                     cudaStream_t s);
-// stage 1 (fused CNN1 + threshold + compaction): a persistent grid of stage1_grid() CTAs,
-// CTA b runs tasks[cta_first[b] .. cta_first[b+1]) (host LPT schedule)
-void launch_stage1(const Cnn1W& w, float T1, const uint8_t* levels, int64_t level_frame_stride,
-                   const LevelInfo* d_levels, const S1Task* d_tasks, const int32_t* d_cta_first,
-                   int grid, S1Cand* cands, uint32_t cand_cap, Ctrl* ctrl, float* dbg_map,
-                   int64_t dbg_map_frame_stride, cudaStream_t s);
+// stage 1 (fused CNN1 + threshold + compaction): a persistent grid of stage1_grid() CTAs
+// taking tasks[0 .. cta_first[grid]) from an atomic counter, longest first
+void launch_stage1(const Cnn1W& w, float T1, const uint8_t* levels, const LevelInfo* d_levels,
+                   const S1Task* d_tasks, const int32_t* d_cta_first, int grid, S1Cand* cands,
+                   uint32_t cand_cap, Ctrl* ctrl, float* dbg_map, cudaStream_t s);
 int stage1_band_width();          // TW of the compiled stage-1 kernel
 int stage1_grid(int sm_count);    // CTAs of the persistent stage-1 launch
 int stage1_task_cost(int nrows);  // relative cost of a task (super-steps)
 // selective unit (stage 2/3), persistent over the survivor queue
 struct SelParams { float T2a, T2b; int32_t Tnn, rule; };
-void launch_selective(const Cnn2W& w2, const Cnn3W& w3, SelParams sp, const uint8_t* frames,
-                      int64_t frame_stride, int64_t pitch, int W, int H, const LevelInfo* d_levels,
-                      const S1Cand* cands, uint32_t cand_cap, SelOut* out, float* dbg_resp,
-                      AccBox* acc, Ctrl* ctrl, int sm_count, cudaStream_t s);
+void launch_selective(const Cnn2W& w2, const Cnn3W& w3, SelParams sp, const FrameInfo* d_frames,
+                      const LevelInfo* d_levels, const S1Cand* cands, uint32_t cand_cap, SelOut* out,
+                      float* dbg_resp, AccBox* acc, Ctrl* ctrl, int sm_count, cudaStream_t s);
 // grouping / NMS per frame + compaction of the results
 void launch_nms(const AccBox* acc, Ctrl* ctrl, int n_frames, int min_cluster, OutBox* staging,
                 int32_t* frame_counts, OutBox* out, cudaStream_t s);

@@ -9,11 +9,13 @@
 // integer arithmetic.
 //
 // Roofline: HBM-bound in principle (the frame read once + 1 B written per level pixel;
-// DESIGN.md "Roofline"), in practice issue-bound on the byte gathers.  A CTA owns a tile
-// of 128 consecutive output columns x 8 rows of one level: each thread loads its column's
-// x-table entry once and walks the rows; the row setup is CTA-uniform; adjacent lanes
-// gather adjacent output pixels (their frame reads stay within 32/sigma bytes) and store
-// one 128-byte line per warp-row; all 8 rows' gathers are issued before any blend.
+// DESIGN.md "Roofline"), in practice issue-bound on the byte gathers.  grid.y = frame,
+// grid.x = tiles of the frame with the most (surplus CTAs of smaller frames exit); a CTA
+// owns a tile of 128 consecutive output columns x 8 rows of one level: each thread loads
+// its column's x-table entry once and walks the rows; the row setup is CTA-uniform;
+// adjacent lanes gather adjacent output pixels (their frame reads stay within 32/sigma
+// bytes) and store one 128-byte line per warp-row; all 8 rows' gathers are issued before
+// any blend.
 // Measured alternatives: 4 adjacent pixels per lane, whole source
 // rows staged in shared memory, one pixel per thread on a flat grid, CTA per output row.
 #include "ccnn_internal.h"
@@ -23,27 +25,29 @@ namespace {
 
 template <bool SAFE>
 __global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
-    const uint8_t* __restrict__ frames, int64_t frame_stride, int64_t pitch, int W, int H,
-    uint8_t* __restrict__ levels, int64_t level_frame_stride,
-    const LevelInfo* __restrict__ lv, int n_levels, const uint32_t* __restrict__ tabs)
+    const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
+    const LevelInfo* __restrict__ lv, const uint32_t* __restrict__ tabs)
 {
-    const int f = blockIdx.y;
-    int l = 0;
-    while (l + 1 < n_levels && lv[l + 1].cta0 <= (int)blockIdx.x) ++l;
+    const FrameInfo F = frames[blockIdx.y];
+    if ((int)blockIdx.x >= F.tiles) return;
+    // level of this tile: linear scan from the frame's largest level (most tiles lie in
+    // the first levels; cta0 is relative to the frame's first level)
+    int l = F.level0;
+    const int l_end = F.level0 + F.nlevels;
+    while (l + 1 < l_end && lv[l + 1].cta0 <= (int)blockIdx.x) ++l;
     const LevelInfo& L = lv[l];
     const int tiles_x = (L.pitch + kPyrCols - 1) / kPyrCols;
     const int t = blockIdx.x - L.cta0;
     const int ty = t / tiles_x, tx = t - ty * tiles_x;
     const int xo = tx * kPyrCols + threadIdx.x;                // output column (pitch-padded)
     if (xo >= L.pitch) return;
-    // SAFE (W, H >= 2): the tables encode the edge so that i1 = i0 + 1 always (runtime.cu
-    // sample_entry); otherwise the clamped form
+    // SAFE (every frame W, H >= 2): the tables encode the edge so that i1 = i0 + 1 always
+    // (runtime.cu sample_entry); otherwise the clamped form
     const uint32_t e = __ldg(tabs + L.tab_off + min(xo, L.lw - 1));   // padding = edge pixel
     const uint32_t x0 = e & 0xFFFFu;
-    const uint32_t x1 = SAFE ? x0 + 1u : min(x0 + 1u, (uint32_t)(W - 1));
+    const uint32_t x1 = SAFE ? x0 + 1u : min(x0 + 1u, (uint32_t)(F.w - 1));
     const int ax = (int)(e >> 16);
-    const uint8_t* src = frames + (int64_t)f * frame_stride;
-    uint8_t* dst = levels + (int64_t)f * level_frame_stride + L.offset + xo;
+    uint8_t* dst = levels + L.offset + xo;
     const uint32_t* yt = tabs + L.tab_off + L.lw;
     const int y_beg = ty * kPyrRows;
     const int nr = min(kPyrRows, L.lh - y_beg);                 // CTA-uniform
@@ -54,10 +58,10 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
     for (int r = 0; r < kPyrRows; ++r) {
         const uint32_t ye = __ldg(yt + y_beg + min(r, nr - 1));
         const uint32_t y0 = ye & 0xFFFFu;
-        const uint32_t y1 = SAFE ? y0 + 1u : min(y0 + 1u, (uint32_t)(H - 1));
+        const uint32_t y1 = SAFE ? y0 + 1u : min(y0 + 1u, (uint32_t)(F.h - 1));
         ay[r] = (int)(ye >> 16);
-        const uint8_t* r0 = src + (int64_t)y0 * pitch;
-        const uint8_t* r1 = src + (int64_t)y1 * pitch;
+        const uint8_t* r0 = F.data + (int64_t)y0 * F.pitch;
+        const uint8_t* r1 = F.data + (int64_t)y1 * F.pitch;
         p[r][0] = __ldg(r0 + x0);
         p[r][1] = __ldg(r0 + x1);
         p[r][2] = __ldg(r1 + x0);
@@ -74,21 +78,16 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
 
 }  // namespace
 
-void launch_pyramid(const uint8_t* frames, int64_t frame_stride, int64_t pitch, int W, int H,
-                    uint8_t* levels, int64_t level_frame_stride, const LevelInfo* d_levels,
-                    const LevelInfo* h_levels, int n_levels, const uint32_t* d_tabs, int n,
+void launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, bool safe,
+                    uint8_t* levels, const LevelInfo* d_levels, const uint32_t* d_tabs,
                     cudaStream_t s)
 {
-    if (n_levels <= 0) return;
-    const LevelInfo& last = h_levels[n_levels - 1];
-    const int tiles = last.cta0 + ((last.pitch + kPyrCols - 1) / kPyrCols) * ((last.lh + kPyrRows - 1) / kPyrRows);
-    dim3 grid(tiles, n);
-    if (W >= 2 && H >= 2)
-        pyramid_kernel<true><<<grid, kPyrCols, 0, s>>>(frames, frame_stride, pitch, W, H, levels,
-                                                       level_frame_stride, d_levels, n_levels, d_tabs);
+    if (n_frames <= 0 || max_tiles <= 0) return;
+    const dim3 grid(max_tiles, n_frames);      // frames of other sizes: surplus CTAs exit
+    if (safe)
+        pyramid_kernel<true><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tabs);
     else
-        pyramid_kernel<false><<<grid, kPyrCols, 0, s>>>(frames, frame_stride, pitch, W, H, levels,
-                                                        level_frame_stride, d_levels, n_levels, d_tabs);
+        pyramid_kernel<false><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tabs);
 }
 
 }  // namespace ccnn

@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <map>
 #include <functional>
 #include <queue>
 
@@ -39,12 +40,13 @@ struct DevBuf {
     template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
-struct PlanKey {
-    int n = -1, W = -1, H = -1, min_face = -1;
+struct PlanKey {                       // batch shape: every frame's size + search settings
+    std::vector<std::pair<int, int>> dims;
+    int min_face = -1;
     float scale_step = 0.f;
     bool operator==(const PlanKey& o) const
     {
-        return n == o.n && W == o.W && H == o.H && min_face == o.min_face && scale_step == o.scale_step;
+        return min_face == o.min_face && scale_step == o.scale_step && dims == o.dims;
     }
 };
 
@@ -80,9 +82,12 @@ struct ccnn_ctx {
     std::vector<int32_t> cta_first;     // stage1_grid + 1 offsets into tasks
     int s1_grid = 0;
     std::vector<uint32_t> tabs;
-    int64_t level_frame_stride = 0;
-    int64_t map_frame_stride = 0;
-    int64_t windows_per_frame = 0;
+    int64_t arena_bytes = 0;            // all levels of all frames
+    int64_t map_total = 0;              // dense stage-1 map floats (debug)
+    int64_t windows_total = 0;
+    int pyr_tiles = 0;                  // largest per-frame pyramid tile count
+    bool all_safe = true;               // every frame W, H >= 2 (pyramid fast path)
+    std::vector<int32_t> frame_level0, frame_nlevels, frame_tiles;
 
     // shared by consecutive batches (their kernels are ordered on the compute stream)
     DevBuf arena, d_levels, d_tasks, d_cta_first, d_tabs, cands, selout, dbg_resp, acc, staging,
@@ -91,6 +96,8 @@ struct ccnn_ctx {
     // per in-flight batch (ccnn_submit / ccnn_collect ping-pong, NEXT #2 streaming ingest)
     struct Slot {
         DevBuf frames;              // H2D destination (host input)
+        DevBuf finfo;               // FrameInfo[n] of the batch
+        FrameInfo* h_finfo = nullptr;   // pinned staging of finfo (max_batch entries)
         DevBuf ctrl, out;           // control block, compacted boxes
         Ctrl* h_ctrl = nullptr;     // pinned readback of ctrl
         cudaEvent_t ev[7] = {};     // h2d0, h2d1, c0, pyramid, stage1, selective, end
@@ -207,46 +214,72 @@ uint32_t sample_entry(int d, double sigma, int n)
     return (uint32_t)f | ((uint32_t)a << 16);
 }
 
-// Level table O1 + stage-1 task table + sampling tables for one batch shape.
-void build_plan(ccnn_ctx* c, int n, int W, int H, int min_face, float scale_step)
+// Level table O1 + stage-1 task table + sampling tables for one batch shape: every frame
+// of the batch gets its own levels (frames may differ in size); the
+// sampling tables are shared by the levels of equally-sized frames.
+void build_plan(ccnn_ctx* c, const PlanKey& key)
 {
     c->levels.clear();
     c->tasks.clear();
     c->tabs.clear();
-    const double sf = (double)scale_step;
-    double s = (double)kWinW / (double)min_face;
-    int64_t off = 0, map_off = 0;
-    int64_t row0 = 0, cta0 = 0;
-    c->windows_per_frame = 0;
-    while (true) {
-        const int lw = (int)std::floor((double)W * s);
-        const int lh = (int)std::floor((double)H * s);
-        if (lw < kWinW || lh < kWinH) break;
-        LevelInfo L{};
-        L.sigma = s;
-        L.lw = lw;
-        L.lh = lh;
-        L.pitch = (int)round_up(lw, 16);
-        L.offset = off;
-        L.nx = (lw - kWinW) / kStep + 1;
-        L.ny = (lh - kWinH) / kStep + 1;
-        L.map_off = (int32_t)map_off;
-        L.tab_off = (int32_t)c->tabs.size();
-        L.row0 = (int32_t)row0;                      // rows of earlier levels
-        L.cta0 = (int32_t)cta0;                      // pyramid tiles of earlier levels
-        cta0 += (int64_t)((L.pitch + kPyrCols - 1) / kPyrCols) * ((lh + kPyrRows - 1) / kPyrRows);
-        for (int x = 0; x < lw; ++x) c->tabs.push_back(sample_entry(x, s, W));
-        for (int y = 0; y < lh; ++y) c->tabs.push_back(sample_entry(y, s, H));
-        off += round_up((int64_t)L.pitch * lh, 256);
-        map_off += (int64_t)L.nx * L.ny;
-        row0 += lh;
-        c->windows_per_frame += (int64_t)L.nx * L.ny;
-        c->levels.push_back(L);
-        s = s / sf;
+    c->frame_level0.clear();
+    c->frame_nlevels.clear();
+    c->frame_tiles.clear();
+    c->pyr_tiles = 0;
+    c->all_safe = true;
+    const double sf = (double)key.scale_step;
+    int64_t off = 0, map_off = 0, cta0 = 0;
+    c->windows_total = 0;
+    std::map<std::pair<int, int>, std::vector<int32_t>> tab_cache;   // (W,H) -> tab_off per level
+    for (int f = 0; f < (int)key.dims.size(); ++f) {
+        const int W = key.dims[f].first, H = key.dims[f].second;
+        auto it = tab_cache.find(key.dims[f]);
+        const bool have_tabs = it != tab_cache.end();
+        std::vector<int32_t> new_tabs;
+        c->frame_level0.push_back((int32_t)c->levels.size());
+        cta0 = 0;                                  // pyramid tiles: per frame (grid.y = frame)
+        double s = (double)kWinW / (double)key.min_face;
+        int k = 0;
+        while (true) {
+            const int lw = (int)std::floor((double)W * s);
+            const int lh = (int)std::floor((double)H * s);
+            if (lw < kWinW || lh < kWinH || k > kMaxLevels) break;   // > kMaxLevels: refused
+            LevelInfo L{};
+            L.sigma = s;
+            L.lw = lw;
+            L.lh = lh;
+            L.pitch = (int)round_up(lw, 16);
+            L.offset = off;
+            L.map_off = map_off;
+            L.nx = (lw - kWinW) / kStep + 1;
+            L.ny = (lh - kWinH) / kStep + 1;
+            L.frame = f;
+            if (have_tabs) {
+                L.tab_off = it->second[k];
+            } else {
+                L.tab_off = (int32_t)c->tabs.size();
+                new_tabs.push_back(L.tab_off);
+                for (int x = 0; x < lw; ++x) c->tabs.push_back(sample_entry(x, s, W));
+                for (int y = 0; y < lh; ++y) c->tabs.push_back(sample_entry(y, s, H));
+            }
+            L.cta0 = (int32_t)cta0;                  // tiles of the frame's earlier levels
+            cta0 += (int64_t)((L.pitch + kPyrCols - 1) / kPyrCols) * ((lh + kPyrRows - 1) / kPyrRows);
+            off += round_up((int64_t)L.pitch * lh, 256);
+            map_off += (int64_t)L.nx * L.ny;
+            c->windows_total += (int64_t)L.nx * L.ny;
+            c->levels.push_back(L);
+            s = s / sf;
+            ++k;
+        }
+        if (!have_tabs) tab_cache[key.dims[f]] = new_tabs;
+        c->frame_nlevels.push_back(k);
+        c->frame_tiles.push_back((int32_t)cta0);
+        c->pyr_tiles = std::max(c->pyr_tiles, (int)cta0);
+        c->all_safe = c->all_safe && W >= 2 && H >= 2;
     }
     // slack so that the stage-1 loader's last (clamped) word read stays in bounds
-    c->level_frame_stride = round_up(off + 256, 256);
-    c->map_frame_stride = map_off;
+    c->arena_bytes = round_up(off + 256, 256);
+    c->map_total = map_off;
     const int TW = stage1_band_width();
     // segment height: the tallest segments (least vertical halo recompute) whose largest
     // task still fits in half the average load of a CTA slot, so the dynamic list schedule
@@ -321,20 +354,13 @@ void build_plan(ccnn_ctx* c, int n, int W, int H, int min_face, float scale_step
                 total += stage1_task_cost(t.nrows);
                 biggest = std::max<int64_t>(biggest, stage1_task_cost(t.nrows));
             }
-            total *= n;
             if (2 * biggest * c->s1_grid <= total) break;
         }
     }
-    // LPT schedule: tasks of all frames, longest first, each to the least-loaded CTA of
-    // the persistent grid (cost ~ super-steps, independent of the band width)
-    std::vector<S1Task> all;
-    all.reserve(one.size() * n);
-    for (int f = 0; f < n; ++f)
-        for (const S1Task& t : one) {
-            S1Task u = t;
-            u.frame = f;
-            all.push_back(u);
-        }
+    // tasks of all frames in one list, longest first (cost ~ super-steps, independent of the
+    // band width); frame = the frame of the first piece (informational)
+    std::vector<S1Task> all = one;
+    for (S1Task& t : all) t.frame = c->levels[t.piece[0].level].frame;
     std::stable_sort(all.begin(), all.end(),
                      [](const S1Task& a, const S1Task& b) { return a.nrows > b.nrows; });
     // the kernel takes tasks in this order from an atomic counter (greedy list scheduling);
@@ -400,6 +426,7 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
     for (auto& sl : ctx->slot) {
         CU(cudaMallocHost(&sl.h_ctrl, sizeof(Ctrl)));
         std::memset(sl.h_ctrl, 0, sizeof(Ctrl));
+        CU(cudaMallocHost(&sl.h_finfo, sizeof(FrameInfo) * (size_t)p->max_batch));
         for (auto& e : sl.ev) CU(cudaEventCreate(&e));
         CU(sl.ctrl.ensure(sizeof(Ctrl)));
     }
@@ -434,6 +461,8 @@ void ccnn_destroy(ccnn_ctx* ctx)
         b->release();
     for (auto& sl : ctx->slot) {
         sl.frames.release();
+        sl.finfo.release();
+        if (sl.h_finfo) cudaFreeHost(sl.h_finfo);
         sl.ctrl.release();
         sl.out.release();
         if (sl.h_ctrl) cudaFreeHost(sl.h_ctrl);
@@ -444,42 +473,55 @@ void ccnn_destroy(ccnn_ctx* ctx)
     delete ctx;
 }
 
-int ccnn_submit(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64_t pitch,
-                int frames_on_device, int min_face, float scale_step, int timed)
+int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frames_on_device,
+                       int min_face, float scale_step, int timed)
 {
     if (!ctx) return CCNN_E_ARG;
     if (!frames) return fail(ctx, CCNN_E_ARG, "NULL frames");
     if (n <= 0 || n > ctx->max_batch) return fail(ctx, CCNN_E_ARG, "n out of [1, max_batch]");
-    if (w < 1 || h < 1 || w > ctx->max_w || h > ctx->max_h)
-        return fail(ctx, CCNN_E_ARG, "frame size out of [1, max_w] x [1, max_h]");
-    if (pitch < w) return fail(ctx, CCNN_E_ARG, "pitch < width");
     if (min_face < 1) return fail(ctx, CCNN_E_ARG, "min_face < 1");
     if (!(scale_step > 1.0f) || !std::isfinite(scale_step))
         return fail(ctx, CCNN_E_ARG, "scale_step must be > 1 (S:227)");
-    if ((double)kWinW / min_face * std::max(w, h) > 32000.0)
-        return fail(ctx, CCNN_E_ARG, "level 0 too large (min_face too small for this frame)");
+    PlanKey key;
+    key.min_face = min_face;
+    key.scale_step = scale_step;
+    key.dims.reserve(n);
+    for (int f = 0; f < n; ++f) {
+        const ccnn_frame& F = frames[f];
+        if (!F.data) return fail(ctx, CCNN_E_ARG, "NULL frame data");
+        if (F.w < 1 || F.h < 1 || F.w > ctx->max_w || F.h > ctx->max_h)
+            return fail(ctx, CCNN_E_ARG, "frame size out of [1, max_w] x [1, max_h]");
+        if (F.pitch < F.w) return fail(ctx, CCNN_E_ARG, "pitch < width");
+        if ((double)kWinW / min_face * std::max(F.w, F.h) > 32000.0)
+            return fail(ctx, CCNN_E_ARG, "level 0 too large (min_face too small for this frame)");
+        key.dims.emplace_back(F.w, F.h);
+    }
     if (ctx->inflight >= 2) return fail(ctx, CCNN_E_STATE, "two batches in flight: ccnn_collect first");
     CU(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
 
-    PlanKey key{n, w, h, min_face, scale_step};
     const bool replan = !(key == ctx->key);
     if (replan) {
         CU(cudaStreamSynchronize(s));              // tables of an in-flight batch stay valid
-        build_plan(ctx, n, w, h, min_face, scale_step);
+        build_plan(ctx, key);
     }
     const int L = (int)ctx->levels.size();
-    if (L > kMaxLevels) {
+    for (int f = 0; f < n; ++f)
+        if (ctx->frame_nlevels[f] > kMaxLevels) {
+            ctx->key = PlanKey{};
+            return fail(ctx, CCNN_E_ARG, "more than 256 pyramid levels (scale_step too close to 1)");
+        }
+    if (L > 32767) {
         ctx->key = PlanKey{};
-        return fail(ctx, CCNN_E_ARG, "more than 256 pyramid levels (scale_step too close to 1)");
+        return fail(ctx, CCNN_E_ARG, "more than 32767 pyramid levels in one batch");
     }
     ccnn_ctx::Slot& sl = ctx->slot[ctx->next_slot];
     sl.n = n;
-    sl.windows = ctx->windows_per_frame * n;
+    sl.windows = ctx->windows_total;
     sl.timed = timed != 0;
     sl.empty = (L == 0);                           // empty pyramid: not an error
-    ctx->last_W = w;
-    ctx->last_H = h;
+    ctx->last_W = frames[0].w;
+    ctx->last_H = frames[0].h;
     if (sl.empty) {
         ctx->key = key;
         sl.cand_cap = 0;
@@ -491,7 +533,7 @@ int ccnn_submit(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
 
     const uint32_t cand_cap = (uint32_t)std::min<int64_t>((int64_t)ctx->queue_cap * n, 0x7FFFFFFF);
     sl.cand_cap = cand_cap;
-    CU(ctx->arena.ensure((size_t)ctx->level_frame_stride * n));
+    CU(ctx->arena.ensure((size_t)ctx->arena_bytes));
     CU(ctx->d_levels.ensure(sizeof(LevelInfo) * L));
     CU(ctx->d_tasks.ensure(sizeof(S1Task) * ctx->tasks.size()));
     CU(ctx->d_cta_first.ensure(sizeof(int32_t) * ctx->cta_first.size()));
@@ -502,12 +544,13 @@ int ccnn_submit(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
     CU(ctx->staging.ensure(sizeof(OutBox) * 2 * kNmsCap * (size_t)n));
     CU(ctx->counts.ensure(sizeof(int32_t) * n));
     CU(sl.out.ensure(sizeof(OutBox) * cand_cap));
+    CU(sl.finfo.ensure(sizeof(FrameInfo) * n));
     const bool dbg1 = (ctx->debug & CCNN_DEBUG_STAGE1) != 0;
     if (dbg1) {
-        CU(ctx->dbg_map.ensure(sizeof(float) * ctx->map_frame_stride * n));
+        CU(ctx->dbg_map.ensure(sizeof(float) * ctx->map_total));
         CU(ctx->dbg_resp.ensure(sizeof(float) * 100 * (size_t)cand_cap));
     }
-    if (replan || ctx->key.n < 0) {
+    if (replan || ctx->key.min_face < 0) {
         CU(cudaMemcpyAsync(ctx->d_levels.p, ctx->levels.data(), sizeof(LevelInfo) * L,
                            cudaMemcpyHostToDevice, s));
         CU(cudaMemcpyAsync(ctx->d_tasks.p, ctx->tasks.data(), sizeof(S1Task) * ctx->tasks.size(),
@@ -522,40 +565,66 @@ int ccnn_submit(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
 
     // ---- frames: device-resident, or H2D on the copy stream (host -> device boundary);
     //      the copy of batch k+1 overlaps the kernels of batch k ----
-    const uint8_t* dframes = frames;
-    int64_t dpitch = pitch;
+    FrameInfo* fi = sl.h_finfo;                    // pinned; reused only after this slot's collect
     if (!frames_on_device) {
-        dpitch = round_up(w, 16);
-        CU(sl.frames.ensure((size_t)dpitch * h * n));
+        std::vector<int64_t> foff(n);
+        int64_t total = 0;
+        for (int f = 0; f < n; ++f) {
+            foff[f] = total;
+            total += round_up(round_up(frames[f].w, 16) * (int64_t)frames[f].h, 256);
+        }
+        CU(sl.frames.ensure((size_t)total));
         // the previous batch of this slot (k-2) read these frames until its end event
         if (sl.used) CU(cudaStreamWaitEvent(ctx->copy_stream, sl.ev[6], 0));
         CU(cudaEventRecord(sl.ev[0], ctx->copy_stream));
-        CU(cudaMemcpy2DAsync(sl.frames.p, dpitch, frames, pitch, w, (size_t)h * n,
-                             cudaMemcpyHostToDevice, ctx->copy_stream));
+        int f = 0;
+        while (f < n) {
+            // one 2-D copy for every run of equally-sized frames laid out back to back
+            int g = f + 1;
+            const int64_t dp = round_up(frames[f].w, 16);
+            while (g < n && frames[g].w == frames[f].w && frames[g].h == frames[f].h &&
+                   frames[g].pitch == frames[f].pitch &&
+                   frames[g].data == frames[f].data + (int64_t)(g - f) * frames[f].h * frames[f].pitch &&
+                   dp * frames[f].h % 256 == 0)
+                ++g;
+            CU(cudaMemcpy2DAsync(sl.frames.as<uint8_t>() + foff[f], dp, frames[f].data, frames[f].pitch,
+                                 frames[f].w, (size_t)frames[f].h * (g - f), cudaMemcpyHostToDevice,
+                                 ctx->copy_stream));
+            for (int q = f; q < g; ++q)
+                fi[q] = FrameInfo{sl.frames.as<uint8_t>() + foff[q], dp, frames[q].w, frames[q].h};
+            f = g;
+        }
         CU(cudaEventRecord(sl.ev[1], ctx->copy_stream));
         CU(cudaStreamWaitEvent(s, sl.ev[1], 0));
-        dframes = sl.frames.as<uint8_t>();
     } else {
+        for (int f = 0; f < n; ++f)
+            fi[f] = FrameInfo{frames[f].data, frames[f].pitch, frames[f].w, frames[f].h};
         CU(cudaEventRecord(sl.ev[0], s));
         CU(cudaEventRecord(sl.ev[1], s));
     }
-    const int64_t fstride = dpitch * h;
+    for (int f = 0; f < n; ++f) {
+        fi[f].level0 = ctx->frame_level0[f];
+        fi[f].nlevels = ctx->frame_nlevels[f];
+        fi[f].tiles = ctx->frame_tiles[f];
+        fi[f].pad = 0;
+    }
+    CU(cudaMemcpyAsync(sl.finfo.p, fi, sizeof(FrameInfo) * n, cudaMemcpyHostToDevice, s));
+    const FrameInfo* dfi = sl.finfo.as<FrameInfo>();
     Ctrl* dctrl = sl.ctrl.as<Ctrl>();
     CU(cudaMemsetAsync(dctrl, 0, sizeof(Ctrl), s));
     CU(cudaEventRecord(sl.ev[2], s));
-    launch_pyramid(dframes, fstride, dpitch, w, h, ctx->arena.as<uint8_t>(), ctx->level_frame_stride,
-                   ctx->d_levels.as<LevelInfo>(), ctx->levels.data(), L, ctx->d_tabs.as<uint32_t>(), n, s);
+    launch_pyramid(dfi, n, ctx->pyr_tiles, ctx->all_safe, ctx->arena.as<uint8_t>(),
+                   ctx->d_levels.as<LevelInfo>(), ctx->d_tabs.as<uint32_t>(), s);
     CU(cudaEventRecord(sl.ev[3], s));
-    launch_stage1(ctx->w1, ctx->T1, ctx->arena.as<uint8_t>(), ctx->level_frame_stride,
-                  ctx->d_levels.as<LevelInfo>(), ctx->d_tasks.as<S1Task>(),
-                  ctx->d_cta_first.as<int32_t>(), (int)ctx->cta_first.size() - 1,
-                  ctx->cands.as<S1Cand>(), cand_cap, dctrl,
-                  dbg1 ? ctx->dbg_map.as<float>() : nullptr, ctx->map_frame_stride, s);
+    launch_stage1(ctx->w1, ctx->T1, ctx->arena.as<uint8_t>(), ctx->d_levels.as<LevelInfo>(),
+                  ctx->d_tasks.as<S1Task>(), ctx->d_cta_first.as<int32_t>(),
+                  (int)ctx->cta_first.size() - 1, ctx->cands.as<S1Cand>(), cand_cap, dctrl,
+                  dbg1 ? ctx->dbg_map.as<float>() : nullptr, s);
     CU(cudaEventRecord(sl.ev[4], s));
-    launch_selective(ctx->w2, ctx->w3, ctx->sp, dframes, fstride, dpitch, w, h,
-                     ctx->d_levels.as<LevelInfo>(), ctx->cands.as<S1Cand>(), cand_cap,
-                     ctx->selout.as<SelOut>(), dbg1 ? ctx->dbg_resp.as<float>() : nullptr,
-                     ctx->acc.as<AccBox>(), dctrl, ctx->sm_count, s);
+    launch_selective(ctx->w2, ctx->w3, ctx->sp, dfi, ctx->d_levels.as<LevelInfo>(),
+                     ctx->cands.as<S1Cand>(), cand_cap, ctx->selout.as<SelOut>(),
+                     dbg1 ? ctx->dbg_resp.as<float>() : nullptr, ctx->acc.as<AccBox>(), dctrl,
+                     ctx->sm_count, s);
     CU(cudaEventRecord(sl.ev[5], s));
     launch_nms(ctx->acc.as<AccBox>(), dctrl, n, ctx->min_cluster, ctx->staging.as<OutBox>(),
                ctx->counts.as<int32_t>(), sl.out.as<OutBox>(), s);
@@ -566,6 +635,17 @@ int ccnn_submit(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
     ctx->next_slot ^= 1;
     ctx->inflight++;
     return CCNN_OK;
+}
+
+int ccnn_submit(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64_t pitch,
+                int frames_on_device, int min_face, float scale_step, int timed)
+{
+    if (!ctx) return CCNN_E_ARG;
+    if (!frames) return fail(ctx, CCNN_E_ARG, "NULL frames");
+    if (n <= 0 || n > ctx->max_batch) return fail(ctx, CCNN_E_ARG, "n out of [1, max_batch]");
+    std::vector<ccnn_frame> fr(n);
+    for (int f = 0; f < n; ++f) fr[f] = ccnn_frame{frames + (int64_t)f * h * pitch, w, h, pitch};
+    return ccnn_submit_frames(ctx, fr.data(), n, frames_on_device, min_face, scale_step, timed);
 }
 
 int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes, ccnn_stats* stats)
@@ -639,6 +719,19 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
     return ccnn_collect(ctx, boxes, box_cap, n_boxes, stats);
 }
 
+int ccnn_detect_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frames_on_device,
+                       int min_face, float scale_step, ccnn_box* boxes, int64_t box_cap,
+                       int64_t* n_boxes, ccnn_stats* stats)
+{
+    if (!ctx) return CCNN_E_ARG;
+    if (!n_boxes || (box_cap > 0 && !boxes)) return fail(ctx, CCNN_E_ARG, "NULL n_boxes / boxes");
+    if (ctx->inflight) return fail(ctx, CCNN_E_STATE, "ccnn_detect_frames with batches in flight");
+    const int rc = ccnn_submit_frames(ctx, frames, n, frames_on_device, min_face, scale_step,
+                                      stats != nullptr);
+    if (rc != CCNN_OK) return rc;
+    return ccnn_collect(ctx, boxes, box_cap, n_boxes, stats);
+}
+
 int ccnn_last_boxes(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes)
 {
     if (!ctx || !n_boxes || (box_cap > 0 && !boxes)) return CCNN_E_ARG;
@@ -655,29 +748,38 @@ int ccnn_last_boxes(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_
     return CCNN_OK;
 }
 
-int ccnn_debug_levels(ccnn_ctx* ctx, double* sigma, int32_t* lw, int32_t* lh, int cap)
+int ccnn_debug_levels(ccnn_ctx* ctx, int frame, double* sigma, int32_t* lw, int32_t* lh, int cap)
 {
     if (!ctx) return CCNN_E_ARG;
-    const int L = (int)ctx->levels.size();
+    if (frame < 0 || frame >= (int)ctx->frame_nlevels.size())
+        return fail(ctx, CCNN_E_ARG, "frame out of range");
+    const int L = ctx->frame_nlevels[frame], l0 = ctx->frame_level0[frame];
     for (int l = 0; l < L && l < cap; ++l) {
-        if (sigma) sigma[l] = ctx->levels[l].sigma;
-        if (lw) lw[l] = ctx->levels[l].lw;
-        if (lh) lh[l] = ctx->levels[l].lh;
+        if (sigma) sigma[l] = ctx->levels[l0 + l].sigma;
+        if (lw) lw[l] = ctx->levels[l0 + l].lw;
+        if (lh) lh[l] = ctx->levels[l0 + l].lh;
     }
     return L;
+}
+
+// the level (frame, level) of the last batch, or nullptr
+static const LevelInfo* debug_level_info(ccnn_ctx* ctx, int frame, int level)
+{
+    if (frame < 0 || frame >= ctx->last_n || frame >= (int)ctx->frame_nlevels.size()) return nullptr;
+    if (level < 0 || level >= ctx->frame_nlevels[frame]) return nullptr;
+    return &ctx->levels[ctx->frame_level0[frame] + level];
 }
 
 int ccnn_debug_level(ccnn_ctx* ctx, int frame, int level, uint8_t* out, int64_t cap)
 {
     if (!ctx || !out) return CCNN_E_ARG;
     if (!ctx->last_valid) return fail(ctx, CCNN_E_STATE, "no completed detect");
-    if (frame < 0 || frame >= ctx->last_n || level < 0 || level >= (int)ctx->levels.size())
-        return fail(ctx, CCNN_E_ARG, "frame/level out of range");
-    const LevelInfo& L = ctx->levels[level];
-    if (cap < (int64_t)L.lw * L.lh) return fail(ctx, CCNN_E_CAPACITY, "cap < lw*lh");
+    const LevelInfo* L = debug_level_info(ctx, frame, level);
+    if (!L) return fail(ctx, CCNN_E_ARG, "frame/level out of range");
+    if (cap < (int64_t)L->lw * L->lh) return fail(ctx, CCNN_E_CAPACITY, "cap < lw*lh");
     CU(cudaSetDevice(ctx->device));
-    CU(cudaMemcpy2DAsync(out, L.lw, ctx->arena.as<uint8_t>() + frame * ctx->level_frame_stride + L.offset,
-                         L.pitch, L.lw, L.lh, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpy2DAsync(out, L->lw, ctx->arena.as<uint8_t>() + L->offset, L->pitch, L->lw, L->lh,
+                         cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return CCNN_OK;
 }
@@ -687,14 +789,13 @@ int ccnn_debug_stage1_map(ccnn_ctx* ctx, int frame, int level, float* out, int64
     if (!ctx || !out) return CCNN_E_ARG;
     if (!ctx->last_valid || !(ctx->debug & CCNN_DEBUG_STAGE1))
         return fail(ctx, CCNN_E_STATE, "needs CCNN_DEBUG_STAGE1 before ccnn_detect");
-    if (frame < 0 || frame >= ctx->last_n || level < 0 || level >= (int)ctx->levels.size())
-        return fail(ctx, CCNN_E_ARG, "frame/level out of range");
-    const LevelInfo& L = ctx->levels[level];
-    const int64_t cnt = (int64_t)L.nx * L.ny;
+    const LevelInfo* L = debug_level_info(ctx, frame, level);
+    if (!L) return fail(ctx, CCNN_E_ARG, "frame/level out of range");
+    const int64_t cnt = (int64_t)L->nx * L->ny;
     if (cap < cnt) return fail(ctx, CCNN_E_CAPACITY, "cap < nx*ny");
     CU(cudaSetDevice(ctx->device));
-    CU(cudaMemcpyAsync(out, ctx->dbg_map.as<float>() + frame * ctx->map_frame_stride + L.map_off,
-                       sizeof(float) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(out, ctx->dbg_map.as<float>() + L->map_off, sizeof(float) * cnt,
+                       cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return CCNN_OK;
 }
@@ -733,7 +834,7 @@ int ccnn_debug_candidates(ccnn_ctx* ctx, ccnn_candidate* out, int64_t cap, int64
         ccnn_candidate& o = out[k];
         std::memset(&o, 0, sizeof(o));
         o.frame = c[k].frame;
-        o.level = c[k].level;
+        o.level = c[k].level - ctx->frame_level0[c[k].frame];   // global -> per-frame id
         o.ix = c[k].ix;
         o.iy = c[k].iy;
         o.s1 = c[k].s1;

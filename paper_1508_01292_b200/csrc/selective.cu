@@ -222,8 +222,7 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
 
 __global__ void __launch_bounds__(kSelThreads, 2) selective_kernel(
     const __grid_constant__ Cnn2W W2, const __grid_constant__ Cnn3W W3, const SelParams sp,
-    const uint8_t* __restrict__ frames, const int64_t frame_stride, const int64_t pitch,
-    const int Wd, const int Hd, const LevelInfo* __restrict__ lvinfo,
+    const FrameInfo* __restrict__ frames, const LevelInfo* __restrict__ lvinfo,
     const S1Cand* __restrict__ cands, const uint32_t cand_cap, SelOut* __restrict__ out,
     float* __restrict__ dbg_resp, AccBox* __restrict__ acc, Ctrl* __restrict__ ctrl)
 {
@@ -240,7 +239,10 @@ __global__ void __launch_bounds__(kSelThreads, 2) selective_kernel(
         if ((uint32_t)ci >= n_cand) break;
         const S1Cand cd = cands[ci];
         const double sigma = lvinfo[cd.level].sigma;
-        const uint8_t* frame = frames + (int64_t)cd.frame * frame_stride;
+        const FrameInfo F = frames[lvinfo[cd.level].frame];
+        const uint8_t* frame = F.data;
+        const int64_t pitch = F.pitch;
+        const int Wd = F.w, Hd = F.h;
 
         // ---- O5 patch geometry, IEEE double, never contracted (bit-identical to the oracle)
         if (tid < kPatchW + kPatchH) {
@@ -396,19 +398,17 @@ size_t selective_smem_bytes()
     return ((sizeof(SelSmem) + 15) & ~size_t(15)) + sizeof(float) * kP1Floats;
 }
 
-void launch_selective(const Cnn2W& w2, const Cnn3W& w3, SelParams sp, const uint8_t* frames,
-                      int64_t frame_stride, int64_t pitch, int W, int H, const LevelInfo* d_levels,
-                      const S1Cand* cands, uint32_t cand_cap, SelOut* out, float* dbg_resp,
-                      AccBox* acc, Ctrl* ctrl, int sm_count, cudaStream_t s)
+void launch_selective(const Cnn2W& w2, const Cnn3W& w3, SelParams sp, const FrameInfo* d_frames,
+                      const LevelInfo* d_levels, const S1Cand* cands, uint32_t cand_cap, SelOut* out,
+                      float* dbg_resp, AccBox* acc, Ctrl* ctrl, int sm_count, cudaStream_t s)
 {
     const size_t smem = selective_smem_bytes();
     cudaFuncSetAttribute(selective_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, selective_kernel, kSelThreads, smem);
     if (occ < 1) occ = 1;
-    selective_kernel<<<sm_count * occ, kSelThreads, smem, s>>>(w2, w3, sp, frames, frame_stride,
-                                                              pitch, W, H, d_levels, cands, cand_cap,
-                                                              out, dbg_resp, acc, ctrl);
+    selective_kernel<<<sm_count * occ, kSelThreads, smem, s>>>(w2, w3, sp, d_frames, d_levels, cands,
+                                                              cand_cap, out, dbg_resp, acc, ctrl);
 }
 
 }  // namespace ccnn

@@ -85,10 +85,10 @@ __device__ __forceinline__ int pmod(int a, int m) { return ((a % m) + m) % m; }
 template <bool DEBUG>
 __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
     const __grid_constant__ Cnn1W W, const float T1,
-    const uint8_t* __restrict__ levels, const int64_t level_frame_stride,
-    const LevelInfo* __restrict__ lvinfo, const S1Task* __restrict__ tasks,
-    const int32_t* __restrict__ cta_first, S1Cand* __restrict__ cands, const uint32_t cand_cap,
-    Ctrl* __restrict__ ctrl, float* __restrict__ dbg_map, const int64_t dbg_map_frame_stride)
+    const uint8_t* __restrict__ levels, const LevelInfo* __restrict__ lvinfo,
+    const S1Task* __restrict__ tasks, const int32_t* __restrict__ cta_first,
+    S1Cand* __restrict__ cands, const uint32_t cand_cap, Ctrl* __restrict__ ctrl,
+    float* __restrict__ dbg_map)
 {
     extern __shared__ __align__(16) float smem[];
     float* const in_ring = smem;
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
             const S1Piece P = piece_of(w);
             const LevelInfo& L = lvinfo[P.level];
             const int lw = min(P.x0 + w - P.J, L.pitch / 4 - 1);
-            const int64_t off = ((int64_t)T.frame * level_frame_stride + L.offset) / 4 + lw;
+            const int64_t off = L.offset / 4 + lw;
             return Src{(uint32_t)off, (uint32_t)(L.pitch / 4) | ((uint32_t)L.lh << 16)};
         };
         auto gword = [&](const Src& sc, int r) -> uint32_t {
@@ -321,8 +321,7 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
                 const float score = act(fmaf(W.w4[1], a1, fmaf(W.w4[0], a0, W.b4)));
                 const bool valid = (o >= 0) && (o < e_rows) && e_col;
                 if (DEBUG && valid)
-                    dbg_map[(int64_t)T.frame * dbg_map_frame_stride + LE.map_off +
-                            (int64_t)(T.y0 + o) * LE.nx + e_x] = score;
+                    dbg_map[LE.map_off + (int64_t)(T.y0 + o) * LE.nx + e_x] = score;
                 const bool pred = valid && (score > T1);             // "exceeded"
                 const unsigned mask = __ballot_sync(0xFFFFFFFFu, pred);
                 if (mask) {
@@ -334,7 +333,7 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
                         const uint32_t idx = base + __popc(mask & ((1u << lane) - 1u));
                         if (idx < cand_cap) {
                             S1Cand cd;
-                            cd.frame = T.frame;
+                            cd.frame = LE.frame;
                             cd.level = (int16_t)e_level;
                             cd.pad = 0;
                             cd.ix = (int16_t)e_x;
@@ -378,22 +377,20 @@ int stage1_grid(int sm_count)
 
 int stage1_task_cost(int nrows) { return (nrows + 7) / 2 + 1 + 2; }   // super-steps + prologue
 
-void launch_stage1(const Cnn1W& w, float T1, const uint8_t* levels, int64_t level_frame_stride,
-                   const LevelInfo* d_levels, const S1Task* d_tasks, const int32_t* d_cta_first,
-                   int grid, S1Cand* cands, uint32_t cand_cap, Ctrl* ctrl, float* dbg_map,
-                   int64_t dbg_map_frame_stride, cudaStream_t s)
+void launch_stage1(const Cnn1W& w, float T1, const uint8_t* levels, const LevelInfo* d_levels,
+                   const S1Task* d_tasks, const int32_t* d_cta_first, int grid, S1Cand* cands,
+                   uint32_t cand_cap, Ctrl* ctrl, float* dbg_map, cudaStream_t s)
 {
     if (grid <= 0) return;
     const size_t smem = sizeof(float) * SMEM_FLOATS;
     if (dbg_map) {
         cudaFuncSetAttribute(stage1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        stage1_kernel<true><<<grid, NT, smem, s>>>(w, T1, levels, level_frame_stride, d_levels, d_tasks,
-                                                   d_cta_first, cands, cand_cap, ctrl, dbg_map,
-                                                   dbg_map_frame_stride);
+        stage1_kernel<true><<<grid, NT, smem, s>>>(w, T1, levels, d_levels, d_tasks, d_cta_first,
+                                                   cands, cand_cap, ctrl, dbg_map);
     } else {
         cudaFuncSetAttribute(stage1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        stage1_kernel<false><<<grid, NT, smem, s>>>(w, T1, levels, level_frame_stride, d_levels, d_tasks,
-                                                    d_cta_first, cands, cand_cap, ctrl, nullptr, 0);
+        stage1_kernel<false><<<grid, NT, smem, s>>>(w, T1, levels, d_levels, d_tasks, d_cta_first,
+                                                    cands, cand_cap, ctrl, nullptr);
     }
 }
 

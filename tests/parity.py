@@ -32,29 +32,53 @@ def oracle_maps(cascade, frames, min_face, scale_step):
     return lv, maps
 
 
+def _oracle_frames(cascade, frames, min_face, scale_step, T1, T2, Tnn, rule):
+    """oracle.detect over a list of frames of individual sizes, frame ids = list index."""
+    cands, boxes, stats = [], [], None
+    for f, fr in enumerate(frames):
+        c, b, st = oracle.detect(cascade, fr[None], min_face, scale_step, T1, T2, Tnn, rule)
+        c["frame"] = f
+        b["frame"] = f
+        cands.append(c)
+        boxes.append(b)
+        stats = st if stats is None else {k: stats[k] + st[k] for k in stats}
+    return np.concatenate(cands), np.concatenate(boxes), stats
+
+
 def compare_run(det, cascade, frames, min_face, scale_step, T1, T2, Tnn, rule, check_maps=True,
                 check_levels=True):
     """Run the GPU detector in debug mode and the oracle on the same frames; assert parity.
-    Returns a Report with the counts and max errors."""
+    `frames`: a uint8 array (n, H, W) (ccnn_detect) or a list of 2-D frames of individual
+    sizes (ccnn_detect_frames).  Returns a Report with the counts and max errors."""
     from paper_1508_01292_b200 import ccnn
-    frames = np.ascontiguousarray(frames, np.uint8)
-    if frames.ndim == 2:
-        frames = frames[None]
     det.set_debug(ccnn.CCNN_DEBUG_STAGE1 | ccnn.CCNN_DEBUG_LEVELS)
-    gboxes = det.detect(frames, min_face, scale_step)
-    gstats = det.last_stats
-    gc = det.candidates()
-    ocands, oboxes, ostats = oracle.detect(cascade, frames, min_face, scale_step, T1, T2, Tnn, rule)
+    if isinstance(frames, (list, tuple)):
+        frames = [np.ascontiguousarray(f, np.uint8) for f in frames]
+        gboxes = det.detect_frames(frames, min_face, scale_step)
+        gstats = det.last_stats
+        gc = det.candidates()
+        ocands, oboxes, ostats = _oracle_frames(cascade, frames, min_face, scale_step, T1, T2,
+                                                Tnn, rule)
+    else:
+        frames = np.ascontiguousarray(frames, np.uint8)
+        if frames.ndim == 2:
+            frames = frames[None]
+        gboxes = det.detect(frames, min_face, scale_step)
+        gstats = det.last_stats
+        gc = det.candidates()
+        ocands, oboxes, ostats = oracle.detect(cascade, frames, min_face, scale_step, T1, T2,
+                                               Tnn, rule)
     rep = Report(n_frames=len(frames))
 
-    # ---- level table and pyramid: exact ----
-    lv = oracle.level_table(frames.shape[2], frames.shape[1], min_face, scale_step)
-    glv = det.levels()
-    assert len(glv) == len(lv)
-    for (gs, gw, gh), (s, w, h) in zip(glv, lv):
-        assert gs == s and gw == w and gh == h
+    # ---- level tables (per frame) and pyramid: exact ----
+    lvs = [oracle.level_table(fr.shape[1], fr.shape[0], min_face, scale_step) for fr in frames]
+    for f, lv in enumerate(lvs):
+        glv = det.levels(f)
+        assert len(glv) == len(lv), f"frame {f}: {len(glv)} levels vs {len(lv)}"
+        for (gs, gw, gh), (s, w, h) in zip(glv, lv):
+            assert gs == s and gw == w and gh == h
     if check_levels:
-        for f in range(len(frames)):
+        for f, lv in enumerate(lvs):
             for l, (s, lw, lh) in enumerate(lv):
                 ref = oracle.resample(frames[f], s, lw, lh)
                 got = det.level_image(f, l)
@@ -64,7 +88,7 @@ def compare_run(det, cascade, frames, min_face, scale_step, T1, T2, Tnn, rule, c
     exempt1 = set()
     max_s1 = 0.0
     if check_maps:
-        for f in range(len(frames)):
+        for f, lv in enumerate(lvs):
             for l, (s, lw, lh) in enumerate(lv):
                 ref = oracle.stage1_dense(cascade.nets[0], oracle.resample(frames[f], s, lw, lh))
                 got = det.stage1_map(f, l).astype(np.float64)

@@ -42,7 +42,7 @@ def test_exports_every_declared_symbol(lib):
     assert declared <= exported, declared - exported
     for name in declared:
         getattr(lib, name)
-    assert lib.ccnn_abi_version() == 1
+    assert lib.ccnn_abi_version() == 2
 
 
 def test_sm100a_code_present():
@@ -57,10 +57,11 @@ def test_struct_layouts_match_header(tmp_path):
 #include <stddef.h>
 #include "ccnn.h"
 int main(void){
- printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(ccnn_layer), sizeof(ccnn_net), sizeof(ccnn_params),
-        sizeof(ccnn_box), sizeof(ccnn_stats), sizeof(ccnn_candidate));
- printf("%zu %zu %zu %zu %zu\\n", offsetof(ccnn_params, T1), offsetof(ccnn_params, Tnn),
-        offsetof(ccnn_params, segment_rows), offsetof(ccnn_stats, ms), offsetof(ccnn_candidate, r3));
+ printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(ccnn_layer), sizeof(ccnn_net), sizeof(ccnn_params),
+        sizeof(ccnn_box), sizeof(ccnn_stats), sizeof(ccnn_candidate), sizeof(ccnn_frame));
+ printf("%zu %zu %zu %zu %zu %zu\\n", offsetof(ccnn_params, T1), offsetof(ccnn_params, Tnn),
+        offsetof(ccnn_params, segment_rows), offsetof(ccnn_stats, ms), offsetof(ccnn_candidate, r3),
+        offsetof(ccnn_frame, pitch));
  return 0;}
 """)
     exe = tmp_path / "sizes"
@@ -69,9 +70,10 @@ int main(void){
     sizes = list(map(int, a.split()))
     offs = list(map(int, b.split()))
     assert sizes == [C.sizeof(ccnn.Layer), C.sizeof(ccnn.Net), C.sizeof(ccnn.Params),
-                     C.sizeof(ccnn.Box), C.sizeof(ccnn.Stats), C.sizeof(ccnn.Candidate)]
+                     C.sizeof(ccnn.Box), C.sizeof(ccnn.Stats), C.sizeof(ccnn.Candidate),
+                     C.sizeof(ccnn.Frame)]
     assert offs == [ccnn.Params.T1.offset, ccnn.Params.Tnn.offset, ccnn.Params.segment_rows.offset,
-                    ccnn.Stats.ms.offset, ccnn.Candidate.r3.offset]
+                    ccnn.Stats.ms.offset, ccnn.Candidate.r3.offset, ccnn.Frame.pitch.offset]
     assert ccnn.BOX_DTYPE.itemsize == C.sizeof(ccnn.Box)
     assert ccnn.CAND_DTYPE.itemsize == C.sizeof(ccnn.Candidate)
 

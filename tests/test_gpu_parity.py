@@ -265,3 +265,68 @@ def test_segment_heights_and_patchwork(ws, cascade, seg):
     rep = parity.compare_run(det, cascade, fr, 96, 1.25, T1, (0.9, 0.2), 2, 0, check_levels=False)
     assert rep["survivors"] > 10
     print(rep)
+
+
+def _quantile_T1_list(cascade, frames, min_face, sf, q):
+    vals = []
+    for fr in frames:
+        _, maps = parity.oracle_maps(cascade, fr[None], min_face, sf)
+        vals += [m.ravel() for m in maps.values()]
+    return float(np.float32(np.quantile(np.concatenate(vals), q)))
+
+
+def _mixed_frames():
+    """stills of individual sizes in one call, including a frame
+    with an empty pyramid in the middle and a 1-pixel-wide one at the end."""
+    return [synth_frames.make_still(333, 257, 991, 20), synth_frames.make_still(450, 450, 992, 20),
+            np.random.default_rng(993).integers(0, 256, (30, 26), dtype=np.uint8), synth_frames.make_still(320, 240, 994, 20),
+            synth_frames.make_still(97, 131, 995, 20), np.full((40, 1), 77, np.uint8)]
+
+
+def test_mixed_size_frames_parity(ws, cascade):
+    fr = _mixed_frames()
+    T1 = _quantile_T1_list(cascade, fr, 20, 1.15, 0.995)
+    T2 = (0.8, 0.1)
+    det = make_det(ws, T1, T2, 1, 0, max_w=640, max_h=480, max_batch=8)
+    rep = parity.compare_run(det, cascade, fr, 20, 1.15, T1, T2, 1, 0)
+    assert rep["survivors"] > 50
+    print(rep)
+
+
+def test_mixed_size_frames_api(ws, cascade):
+    """detect_frames == one detect per frame; host, pinned, device and pitched device frames
+    agree; submit_frames interleaves with submit; replans between shapes are exact."""
+    import torch
+    fr = _mixed_frames()
+    T1, T2 = _quantile_T1_list(cascade, fr, 20, 1.15, 0.99), (0.8, 0.1)
+    det = make_det(ws, T1, T2, 1, 0, max_w=640, max_h=480, max_batch=8)
+    per = []
+    for f, x in enumerate(fr):
+        b = det.detect(x[None], 20, 1.15)
+        b["frame"] = f
+        per.append(b)
+    ref = np.concatenate(per)
+    a = det.detect_frames(fr, 20, 1.15)
+    assert np.array_equal(a, ref)
+    pinned = [torch.from_numpy(x).pin_memory() for x in fr]
+    assert np.array_equal(det.detect_frames(pinned, 20, 1.15), ref)
+    dev = []
+    for x in fr:                                       # pitched device views
+        big = torch.zeros((x.shape[0], x.shape[1] + 37), dtype=torch.uint8, device="cuda")
+        big[:, :x.shape[1]] = torch.from_numpy(x).cuda()
+        dev.append(big[:, :x.shape[1]])
+    assert np.array_equal(det.detect_frames(dev, 20, 1.15), ref)
+    # streaming: alternate frame lists and uniform batches, two in flight
+    uni = np.stack([fr[0], fr[0]])
+    det.submit_frames(pinned, 20, 1.15)
+    det.submit(uni, 20, 1.15)
+    g0 = det.collect()
+    det.submit_frames(fr[::-1], 20, 1.15)
+    g1 = det.collect()
+    g2 = det.collect()
+    assert np.array_equal(g0, ref)
+    u = det.detect(uni, 20, 1.15)
+    assert np.array_equal(g1, u)
+    rev = np.concatenate([per[len(fr) - 1 - k] for k in range(len(fr))])
+    rev["frame"] = np.repeat(np.arange(len(fr)), [len(per[len(fr) - 1 - k]) for k in range(len(fr))])
+    assert np.array_equal(g2, rev)
