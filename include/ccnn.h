@@ -183,6 +183,7 @@ int ccnn_abi_version(void);
  * ---------------------------------------------------------------------------------- */
 #define CCNN_DEBUG_LEVELS   1  /* keep the pyramid levels (already resident)        */
 #define CCNN_DEBUG_STAGE1   2  /* also write every stage-1 response to a dense map */
+#define CCNN_DEBUG_PYR_TEX  4  /* pyramid by texture gathers (tld4), not byte gathers */
 int ccnn_set_debug(ccnn_ctx* ctx, int flags);
 
 /* Level table of frame `frame` of the last submitted batch: up to cap levels, returns

@@ -16,7 +16,7 @@ if os.environ.get("CCNN_LIB_VARIANT"):      # experiments only: an in-tree varia
 
 CCNN_OK, CCNN_E_ARG, CCNN_E_ARCH, CCNN_E_WEIGHTS = 0, -1, -2, -3
 CCNN_E_CAPACITY, CCNN_E_QUEUE, CCNN_E_CUDA, CCNN_E_STATE = -4, -5, -6, -7
-CCNN_DEBUG_LEVELS, CCNN_DEBUG_STAGE1 = 1, 2
+CCNN_DEBUG_LEVELS, CCNN_DEBUG_STAGE1, CCNN_DEBUG_PYR_TEX = 1, 2, 4
 
 # every entry point declared in include/ccnn.h
 EXPORTS = ("ccnn_create", "ccnn_set_stream", "ccnn_detect", "ccnn_detect_frames",

@@ -44,7 +44,9 @@ struct FrameInfo {             // one frame of a batch, as the kernels read it
     int64_t pitch;             // row pitch in bytes
     int32_t w, h;
     int32_t level0, nlevels;   // its levels: LevelInfo[level0 .. level0 + nlevels)
-    int32_t tiles, pad;        // pyramid tiles of all its levels
+    int32_t tiles, tile_off;   // pyramid tiles of all its levels; their descriptors at
+                               // tiles[tile_off ..] (shared by equally-sized frames)
+    unsigned long long tex;    // pitch-2D uint8 texture object over data (0 = none)
 };
 struct LevelInfo {             // one pyramid level of one frame of the batch
     double sigma;
@@ -52,12 +54,19 @@ struct LevelInfo {             // one pyramid level of one frame of the batch
     int64_t map_off;           // offset of the level in the dense stage-1 map (debug)
     int32_t lw, lh, pitch;     // level size, row pitch (multiple of 16 B)
     int32_t nx, ny;            // window grid
-    int32_t tab_off;           // offset of the level's x table (lw entries) then y table (lh)
+    int32_t tab_off;           // offset of the level's x table (pitch entries) then y table
+                               // (lh rounded up to kPyrTileRows entries); multiple of 4
     int32_t frame;             // the frame this level belongs to
-    int32_t cta0;              // pyramid tiles (kPyrCols x kPyrRows) of the earlier levels of its frame
+    int32_t pad0;
     int32_t pad;
 };
-constexpr int kPyrCols = 128, kPyrRows = 8;   // pyramid CTA tile
+// pyramid CTA tile: kPyrCols output columns x kPyrGroups groups of kPyrRows rows of one
+// level; descriptor = level-in-frame | tile column << 8 | tile row << 16
+#ifndef PYR_ROWS
+#define PYR_ROWS 8
+#endif
+constexpr int kPyrCols = 128, kPyrRows = PYR_ROWS, kPyrGroups = 32 / PYR_ROWS;
+constexpr int kPyrTileRows = kPyrRows * kPyrGroups;
 
 // One stage-1 CTA task: a band of TW = 59 window columns x a segment of rows.  Patchwork
 // (SURVEY §8(f) NEXT #1): a band holds up to kMaxPieces pieces of levels
@@ -110,9 +119,10 @@ constexpr int kNmsCap = 4096;  // raw boxes per frame handled by one NMS CTA
 
 // ---- launchers (stream-ordered, no sync) ----
 // pyramid: every level of every frame, from the original frames
+// use_tex: every frame has a texture object (FrameInfo.tex): 2x2 footprints by tex2Dgather
 void launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, bool safe,
-                    uint8_t* levels, const LevelInfo* d_levels, const uint32_t* d_tabs,
-                    cudaStream_t s);
+                    bool use_tex, uint8_t* levels, const LevelInfo* d_levels,
+                    const uint32_t* d_tiles, const uint32_t* d_tabs, cudaStream_t s);
 // stage 1 (fused CNN1 + threshold + compaction): a persistent grid of stage1_grid() CTAs
 // taking tasks[0 .. cta_first[grid]) from an atomic counter, longest first
 void launch_stage1(const Cnn1W& w, float T1, const uint8_t* levels, const LevelInfo* d_levels,

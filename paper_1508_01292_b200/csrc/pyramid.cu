@@ -9,85 +9,171 @@
 // integer arithmetic.
 //
 // Roofline: HBM-bound in principle (the frame read once + 1 B written per level pixel;
-// DESIGN.md "Roofline"), in practice issue-bound on the byte gathers.  grid.y = frame,
-// grid.x = tiles of the frame with the most (surplus CTAs of smaller frames exit); a CTA
-// owns a tile of 128 consecutive output columns x 8 rows of one level: each thread loads
-// its column's x-table entry once and walks the rows; the row setup is CTA-uniform;
-// adjacent lanes gather adjacent output pixels (their frame reads stay within 32/sigma
-// bytes) and store one 128-byte line per warp-row; all 8 rows' gathers are issued before
-// any blend.
-// Measured alternatives: 4 adjacent pixels per lane, whole source
-// rows staged in shared memory, one pixel per thread on a flat grid, CTA per output row.
+// DESIGN.md "Roofline"), in practice issue-bound (integer ALU).  grid.y = frame, grid.x =
+// tiles of the frame with the most (surplus CTAs of smaller frames exit).  A CTA owns a
+// tile of 128 consecutive output columns x 32 rows of one level, found through a host-built
+// descriptor (no per-CTA search or division); each thread loads its column's x-table entry
+// once and walks the rows in groups of 8 whose fetches are all issued before any blend;
+// adjacent lanes fetch adjacent output pixels (their frame reads stay within 32/sigma bytes)
+// and store one 32-byte sector per warp-row.
+// Two fetch forms, identical results: four byte gathers (default), or tld4 texture
+// gathers (the 2x2 footprint in one instruction, hardware 2-D addressing -- the paper's
+// texture pyramid) on request (CCNN_DEBUG_PYR_TEX) when every frame has a texture
+// object.  Measured at C4: 0.265 ms byte gathers vs 0.288 ms tld4 (tex_throttle-bound).
 #include "ccnn_internal.h"
 
 namespace ccnn {
 namespace {
 
+struct PyrTile {
+    const LevelInfo* L;
+    int xo, y_beg, nr;     // output column, first row, rows of this tile (<= kPyrTileRows)
+};
+
+// decode this CTA's tile; false if the thread has no column
+__device__ __forceinline__ bool pyr_tile(const FrameInfo& F, const LevelInfo* __restrict__ lv,
+                                         const uint32_t* __restrict__ tiles, PyrTile& T)
+{
+    const uint32_t d = __ldg(tiles + F.tile_off + blockIdx.x);
+    T.L = lv + F.level0 + (int)(d & 0xFFu);
+    T.xo = (int)((d >> 8) & 0xFFu) * kPyrCols + threadIdx.x;
+    T.y_beg = (int)(d >> 16) * kPyrTileRows;
+    T.nr = min(kPyrTileRows, T.L->lh - T.y_beg);
+    return T.xo < T.L->pitch;
+}
+
+// p0*(2048-a) + p1*a == (p0 << 11) + (p1 - p0)*a, exactly (O2)
+__device__ __forceinline__ uint8_t blend(int p00, int p01, int p10, int p11, int ax, int ay)
+{
+    const int top = (p00 << 11) + (p01 - p00) * ax;
+    const int bot = (p10 << 11) + (p11 - p10) * ax;
+    return (uint8_t)(((top << 11) + (bot - top) * ay + (1 << 21)) >> 22);
+}
+
+// the y-table entries of a row group: 16-B loads (the table is padded and aligned,
+// runtime.cu build_plan), the same address across the CTA
+__device__ __forceinline__ void load_rows(const uint32_t* __restrict__ yt, uint32_t (&ye)[kPyrRows])
+{
+#pragma unroll
+    for (int k = 0; k < kPyrRows / 4; ++k) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(yt) + k);
+        ye[4 * k + 0] = a.x; ye[4 * k + 1] = a.y; ye[4 * k + 2] = a.z; ye[4 * k + 3] = a.w;
+    }
+}
+
 template <bool SAFE>
 __global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
     const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
-    const LevelInfo* __restrict__ lv, const uint32_t* __restrict__ tabs)
+    const LevelInfo* __restrict__ lv, const uint32_t* __restrict__ tiles,
+    const uint32_t* __restrict__ tabs)
 {
     const FrameInfo F = frames[blockIdx.y];
     if ((int)blockIdx.x >= F.tiles) return;
-    // level of this tile: linear scan from the frame's largest level (most tiles lie in
-    // the first levels; cta0 is relative to the frame's first level)
-    int l = F.level0;
-    const int l_end = F.level0 + F.nlevels;
-    while (l + 1 < l_end && lv[l + 1].cta0 <= (int)blockIdx.x) ++l;
-    const LevelInfo& L = lv[l];
-    const int tiles_x = (L.pitch + kPyrCols - 1) / kPyrCols;
-    const int t = blockIdx.x - L.cta0;
-    const int ty = t / tiles_x, tx = t - ty * tiles_x;
-    const int xo = tx * kPyrCols + threadIdx.x;                // output column (pitch-padded)
-    if (xo >= L.pitch) return;
+    PyrTile T;
+    if (!pyr_tile(F, lv, tiles, T)) return;
+    const LevelInfo& L = *T.L;
     // SAFE (every frame W, H >= 2): the tables encode the edge so that i1 = i0 + 1 always
     // (runtime.cu sample_entry); otherwise the clamped form
-    const uint32_t e = __ldg(tabs + L.tab_off + min(xo, L.lw - 1));   // padding = edge pixel
+    const uint32_t e = __ldg(tabs + L.tab_off + T.xo);          // padding = edge column
     const uint32_t x0 = e & 0xFFFFu;
     const uint32_t x1 = SAFE ? x0 + 1u : min(x0 + 1u, (uint32_t)(F.w - 1));
     const int ax = (int)(e >> 16);
-    uint8_t* dst = levels + L.offset + xo;
-    const uint32_t* yt = tabs + L.tab_off + L.lw;
-    const int y_beg = ty * kPyrRows;
-    const int nr = min(kPyrRows, L.lh - y_beg);                 // CTA-uniform
-    // all rows' table entries and frame bytes are loaded before any blend: 8 rows of
-    // independent gathers in flight per thread
-    int p[kPyrRows][4], ay[kPyrRows];
+    const int pitch = L.pitch;
+    uint8_t* dst = levels + L.offset + T.xo + (int64_t)T.y_beg * pitch;
+    const uint32_t* yt = tabs + L.tab_off + pitch + T.y_beg;   // padded: no clamp
+    for (int g0 = 0; g0 < T.nr; g0 += kPyrRows) {             // CTA-uniform
+        const int nr = T.nr - g0;
+        uint32_t ye[kPyrRows];
+        load_rows(yt + g0, ye);
+        int p[kPyrRows][4];
 #pragma unroll
-    for (int r = 0; r < kPyrRows; ++r) {
-        const uint32_t ye = __ldg(yt + y_beg + min(r, nr - 1));
-        const uint32_t y0 = ye & 0xFFFFu;
-        const uint32_t y1 = SAFE ? y0 + 1u : min(y0 + 1u, (uint32_t)(F.h - 1));
-        ay[r] = (int)(ye >> 16);
-        const uint8_t* r0 = F.data + (int64_t)y0 * F.pitch;
-        const uint8_t* r1 = F.data + (int64_t)y1 * F.pitch;
-        p[r][0] = __ldg(r0 + x0);
-        p[r][1] = __ldg(r0 + x1);
-        p[r][2] = __ldg(r1 + x0);
-        p[r][3] = __ldg(r1 + x1);
+        for (int r = 0; r < kPyrRows; ++r) {
+            const uint32_t y0 = ye[r] & 0xFFFFu;
+            const uint32_t y1 = SAFE ? y0 + 1u : min(y0 + 1u, (uint32_t)(F.h - 1));
+            const uint8_t* r0 = F.data + (int64_t)y0 * F.pitch;
+            const uint8_t* r1 = F.data + (int64_t)y1 * F.pitch;
+            p[r][0] = __ldg(r0 + x0);
+            p[r][1] = __ldg(r0 + x1);
+            p[r][2] = __ldg(r1 + x0);
+            p[r][3] = __ldg(r1 + x1);
+        }
+        uint8_t* d = dst + (int64_t)g0 * pitch;
+        if (nr >= kPyrRows) {
+#pragma unroll
+            for (int r = 0; r < kPyrRows; ++r)
+                d[r * pitch] = blend(p[r][0], p[r][1], p[r][2], p[r][3], ax, (int)(ye[r] >> 16));
+        } else {
+#pragma unroll
+            for (int r = 0; r < kPyrRows; ++r)
+                if (r < nr) d[r * pitch] = blend(p[r][0], p[r][1], p[r][2], p[r][3], ax, (int)(ye[r] >> 16));
+        }
     }
+}
+
+// tld4 (texture gather, red channel) with an integer destination type: the four texels of
+// the 2x2 footprint at unnormalised (u, v) as zero-extended u32 -- order (i0, j1), (i1, j1),
+// (i1, j0), (i0, j0) for the footprint at (i0 + 1, j0 + 1); clamp addressing supplies
+// i1 = min(i0 + 1, W - 1)
+__device__ __forceinline__ void gather4(cudaTextureObject_t tex, float u, float v, uint32_t& a,
+                                        uint32_t& b, uint32_t& c, uint32_t& d)
+{
+    asm volatile("tld4.r.2d.v4.u32.f32 {%0, %1, %2, %3}, [%4, {%5, %6}];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "l"(tex), "f"(u), "f"(v));
+}
+
+__global__ void __launch_bounds__(kPyrCols) pyramid_tex_kernel(
+    const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
+    const LevelInfo* __restrict__ lv, const uint32_t* __restrict__ tiles,
+    const uint32_t* __restrict__ tabs)
+{
+    const FrameInfo F = frames[blockIdx.y];
+    if ((int)blockIdx.x >= F.tiles) return;
+    PyrTile T;
+    if (!pyr_tile(F, lv, tiles, T)) return;
+    const LevelInfo& L = *T.L;
+    const uint32_t e = __ldg(tabs + L.tab_off + T.xo);
+    const float u = (float)(e & 0xFFFFu) + 1.0f;
+    const int ax = (int)(e >> 16);
+    const cudaTextureObject_t tex = (cudaTextureObject_t)F.tex;
+    const int pitch = L.pitch;
+    uint8_t* dst = levels + L.offset + T.xo + (int64_t)T.y_beg * pitch;
+    const uint32_t* yt = tabs + L.tab_off + pitch + T.y_beg;
+    for (int g0 = 0; g0 < T.nr; g0 += kPyrRows) {             // CTA-uniform
+        const int nr = T.nr - g0;
+        uint32_t ye[kPyrRows];
+        load_rows(yt + g0, ye);
+        uint32_t q[kPyrRows][4];
 #pragma unroll
-    for (int r = 0; r < kPyrRows; ++r) {
-        // p0*(2048-a) + p1*a == (p0 << 11) + (p1 - p0)*a, exactly (O2)
-        const int top = (p[r][0] << 11) + (p[r][1] - p[r][0]) * ax;
-        const int bot = (p[r][2] << 11) + (p[r][3] - p[r][2]) * ax;
-        if (r < nr) dst[(int64_t)(y_beg + r) * L.pitch] = (uint8_t)(((top << 11) + (bot - top) * ay[r] + (1 << 21)) >> 22);
+        for (int r = 0; r < kPyrRows; ++r)
+            gather4(tex, u, (float)(ye[r] & 0xFFFFu) + 1.0f, q[r][0], q[r][1], q[r][2], q[r][3]);
+        uint8_t* d = dst + (int64_t)g0 * pitch;
+        if (nr >= kPyrRows) {
+#pragma unroll
+            for (int r = 0; r < kPyrRows; ++r)
+                d[r * pitch] = blend(q[r][3], q[r][2], q[r][0], q[r][1], ax, (int)(ye[r] >> 16));
+        } else {
+#pragma unroll
+            for (int r = 0; r < kPyrRows; ++r)
+                if (r < nr) d[r * pitch] = blend(q[r][3], q[r][2], q[r][0], q[r][1], ax, (int)(ye[r] >> 16));
+        }
     }
 }
 
 }  // namespace
 
 void launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, bool safe,
-                    uint8_t* levels, const LevelInfo* d_levels, const uint32_t* d_tabs,
-                    cudaStream_t s)
+                    bool use_tex, uint8_t* levels, const LevelInfo* d_levels,
+                    const uint32_t* d_tiles, const uint32_t* d_tabs, cudaStream_t s)
 {
     if (n_frames <= 0 || max_tiles <= 0) return;
     const dim3 grid(max_tiles, n_frames);      // frames of other sizes: surplus CTAs exit
-    if (safe)
-        pyramid_kernel<true><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tabs);
+    if (use_tex)
+        pyramid_tex_kernel<<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
+    else if (safe)
+        pyramid_kernel<true><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
     else
-        pyramid_kernel<false><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tabs);
+        pyramid_kernel<false><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
 }
 
 }  // namespace ccnn

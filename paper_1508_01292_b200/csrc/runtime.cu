@@ -12,6 +12,7 @@
 #include <vector>
 #include <algorithm>
 #include <map>
+#include <tuple>
 #include <functional>
 #include <queue>
 
@@ -87,10 +88,11 @@ struct ccnn_ctx {
     int64_t windows_total = 0;
     int pyr_tiles = 0;                  // largest per-frame pyramid tile count
     bool all_safe = true;               // every frame W, H >= 2 (pyramid fast path)
-    std::vector<int32_t> frame_level0, frame_nlevels, frame_tiles;
+    std::vector<int32_t> frame_level0, frame_nlevels, frame_tiles, frame_tile_off;
+    std::vector<uint32_t> ptiles;       // pyramid tile descriptors (pyramid.cu)
 
     // shared by consecutive batches (their kernels are ordered on the compute stream)
-    DevBuf arena, d_levels, d_tasks, d_cta_first, d_tabs, cands, selout, dbg_resp, acc, staging,
+    DevBuf arena, d_levels, d_tasks, d_cta_first, d_tabs, d_ptiles, cands, selout, dbg_resp, acc, staging,
         counts, dbg_map;
 
     // per in-flight batch (ccnn_submit / ccnn_collect ping-pong, NEXT #2 streaming ingest)
@@ -109,6 +111,10 @@ struct ccnn_ctx {
     } slot[2];
     cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
     int next_slot = 0, inflight = 0;
+
+    // texture objects over frames (pyramid tex2Dgather path), keyed by (data, w, h, pitch)
+    std::map<std::tuple<uintptr_t, int, int, int64_t>, cudaTextureObject_t> tex_cache;
+    int tex_align = 512, tex_pitch_align = 32;
 
     // last collected batch (test hooks, ccnn_last_boxes)
     int last_slot = 0;
@@ -199,6 +205,52 @@ void unpack_sel(const float* p, SelNetW<A, B, C>& o)
 
 int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
+// Texture object over one uint8 frame (pitch-2D, point sampling, clamp-to-edge, unnormalised
+// coordinates), cached; 0 if the frame's address or pitch does not meet the texture
+// alignment (the pyramid then takes its byte-gather form).
+cudaTextureObject_t frame_texture(ccnn_ctx* c, const uint8_t* data, int w, int h, int64_t pitch)
+{
+    if ((uintptr_t)data % c->tex_align || pitch % c->tex_pitch_align) return 0;
+    const auto key = std::make_tuple((uintptr_t)data, w, h, pitch);
+    auto it = c->tex_cache.find(key);
+    if (it != c->tex_cache.end()) return it->second;
+    cudaResourceDesc rd{};
+    rd.resType = cudaResourceTypePitch2D;
+    rd.res.pitch2D.devPtr = const_cast<uint8_t*>(data);
+    rd.res.pitch2D.desc = cudaCreateChannelDesc<unsigned char>();
+    rd.res.pitch2D.width = (size_t)w;
+    rd.res.pitch2D.height = (size_t)h;
+    rd.res.pitch2D.pitchInBytes = (size_t)pitch;
+    cudaTextureDesc td{};
+    td.addressMode[0] = cudaAddressModeClamp;
+    td.addressMode[1] = cudaAddressModeClamp;
+    td.filterMode = cudaFilterModePoint;
+    td.readMode = cudaReadModeElementType;
+    td.normalizedCoords = 0;
+    cudaTextureObject_t t = 0;
+    if (cudaCreateTextureObject(&t, &rd, &td, nullptr) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    c->tex_cache.emplace(key, t);
+    return t;
+}
+
+// destroy cached texture objects whose frame lies in [lo, lo + bytes) (all if bytes == 0);
+// the caller guarantees no queued kernel still uses them
+void drop_textures(ccnn_ctx* c, const void* lo, size_t bytes)
+{
+    for (auto it = c->tex_cache.begin(); it != c->tex_cache.end();) {
+        const uintptr_t p = std::get<0>(it->first);
+        if (bytes == 0 || (p >= (uintptr_t)lo && p < (uintptr_t)lo + bytes)) {
+            cudaDestroyTextureObject(it->second);
+            it = c->tex_cache.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
 // O2 sampling table entry: s = (d + 0.5)/sigma - 0.5, clamp [0, n-1], i0 = floor(s),
 // i1 = min(i0 + 1, n - 1), a = floor((s - i0) * 2048 + 0.5); packed i0 | a << 16.
 // For n >= 2 the clamped edge (i0 = n-1, a = 0) is re-encoded as (i0 = n-2, a = 2048):
@@ -225,19 +277,22 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
     c->frame_level0.clear();
     c->frame_nlevels.clear();
     c->frame_tiles.clear();
+    c->frame_tile_off.clear();
+    c->ptiles.clear();
     c->pyr_tiles = 0;
     c->all_safe = true;
     const double sf = (double)key.scale_step;
-    int64_t off = 0, map_off = 0, cta0 = 0;
+    int64_t off = 0, map_off = 0;
     c->windows_total = 0;
     std::map<std::pair<int, int>, std::vector<int32_t>> tab_cache;   // (W,H) -> tab_off per level
+    std::map<std::pair<int, int>, std::pair<int32_t, int32_t>> tile_cache;   // -> (offset, count)
     for (int f = 0; f < (int)key.dims.size(); ++f) {
         const int W = key.dims[f].first, H = key.dims[f].second;
         auto it = tab_cache.find(key.dims[f]);
         const bool have_tabs = it != tab_cache.end();
         std::vector<int32_t> new_tabs;
         c->frame_level0.push_back((int32_t)c->levels.size());
-        cta0 = 0;                                  // pyramid tiles: per frame (grid.y = frame)
+        const int level0 = (int)c->levels.size();
         double s = (double)kWinW / (double)key.min_face;
         int k = 0;
         while (true) {
@@ -259,11 +314,13 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
             } else {
                 L.tab_off = (int32_t)c->tabs.size();
                 new_tabs.push_back(L.tab_off);
-                for (int x = 0; x < lw; ++x) c->tabs.push_back(sample_entry(x, s, W));
-                for (int y = 0; y < lh; ++y) c->tabs.push_back(sample_entry(y, s, H));
+                // x entries for every pitch column (padding repeats the edge column), then
+                // y entries for kPyrTileRows-rounded rows (padding repeats the last row): the
+                // pyramid kernel reads them unclamped; 16-B aligned (pitch % 16 == 0)
+                for (int x = 0; x < L.pitch; ++x) c->tabs.push_back(sample_entry(std::min(x, lw - 1), s, W));
+                const int lh_pad = (int)round_up(lh, kPyrTileRows);
+                for (int y = 0; y < lh_pad; ++y) c->tabs.push_back(sample_entry(std::min(y, lh - 1), s, H));
             }
-            L.cta0 = (int32_t)cta0;                  // tiles of the frame's earlier levels
-            cta0 += (int64_t)((L.pitch + kPyrCols - 1) / kPyrCols) * ((lh + kPyrRows - 1) / kPyrRows);
             off += round_up((int64_t)L.pitch * lh, 256);
             map_off += (int64_t)L.nx * L.ny;
             c->windows_total += (int64_t)L.nx * L.ny;
@@ -271,10 +328,26 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
             s = s / sf;
             ++k;
         }
-        if (!have_tabs) tab_cache[key.dims[f]] = new_tabs;
         c->frame_nlevels.push_back(k);
-        c->frame_tiles.push_back((int32_t)cta0);
-        c->pyr_tiles = std::max(c->pyr_tiles, (int)cta0);
+        // pyramid tile descriptors (level-in-frame | tile column << 8 | tile row << 16),
+        // largest levels first; shared by equally-sized frames
+        if (!have_tabs) {
+            tab_cache[key.dims[f]] = new_tabs;
+            tile_cache[key.dims[f]] = {(int32_t)c->ptiles.size(), 0};
+            for (int l = 0; l < k && l < 256; ++l) {
+                const LevelInfo& L = c->levels[level0 + l];
+                const int tx_n = (L.pitch + kPyrCols - 1) / kPyrCols;
+                const int ty_n = (L.lh + kPyrTileRows - 1) / kPyrTileRows;
+                for (int ty = 0; ty < ty_n; ++ty)
+                    for (int tx = 0; tx < tx_n; ++tx)
+                        c->ptiles.push_back((uint32_t)l | ((uint32_t)tx << 8) | ((uint32_t)ty << 16));
+            }
+            tile_cache[key.dims[f]].second = (int32_t)c->ptiles.size() - tile_cache[key.dims[f]].first;
+        }
+        const auto tc = tile_cache[key.dims[f]];
+        c->frame_tile_off.push_back(tc.first);
+        c->frame_tiles.push_back(tc.second);
+        c->pyr_tiles = std::max(c->pyr_tiles, tc.second);
         c->all_safe = c->all_safe && W >= 2 && H >= 2;
     }
     // slack so that the stage-1 loader's last (clamped) word read stays in bounds
@@ -430,6 +503,10 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
         for (auto& e : sl.ev) CU(cudaEventCreate(&e));
         CU(sl.ctrl.ensure(sizeof(Ctrl)));
     }
+    CU(cudaDeviceGetAttribute(&ctx->tex_align, cudaDevAttrTextureAlignment, cuda_device));
+    CU(cudaDeviceGetAttribute(&ctx->tex_pitch_align, cudaDevAttrTexturePitchAlignment, cuda_device));
+    ctx->tex_align = std::max(ctx->tex_align, 1);
+    ctx->tex_pitch_align = std::max(ctx->tex_pitch_align, 1);
     CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
     *out = ctx;
@@ -455,7 +532,8 @@ void ccnn_destroy(ccnn_ctx* ctx)
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
-    for (DevBuf* b : {&ctx->arena, &ctx->d_levels, &ctx->d_tasks, &ctx->d_cta_first, &ctx->d_tabs,
+    drop_textures(ctx, nullptr, 0);
+    for (DevBuf* b : {&ctx->arena, &ctx->d_levels, &ctx->d_tasks, &ctx->d_cta_first, &ctx->d_tabs, &ctx->d_ptiles,
                       &ctx->cands, &ctx->selout, &ctx->dbg_resp, &ctx->acc, &ctx->staging, &ctx->counts,
                       &ctx->dbg_map})
         b->release();
@@ -538,6 +616,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     CU(ctx->d_tasks.ensure(sizeof(S1Task) * ctx->tasks.size()));
     CU(ctx->d_cta_first.ensure(sizeof(int32_t) * ctx->cta_first.size()));
     CU(ctx->d_tabs.ensure(sizeof(uint32_t) * ctx->tabs.size()));
+    CU(ctx->d_ptiles.ensure(sizeof(uint32_t) * std::max<size_t>(1, ctx->ptiles.size())));
     CU(ctx->cands.ensure(sizeof(S1Cand) * cand_cap));
     CU(ctx->selout.ensure(sizeof(SelOut) * cand_cap));
     CU(ctx->acc.ensure(sizeof(AccBox) * cand_cap));
@@ -557,6 +636,9 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
                            cudaMemcpyHostToDevice, s));
         CU(cudaMemcpyAsync(ctx->d_tabs.p, ctx->tabs.data(), sizeof(uint32_t) * ctx->tabs.size(),
                            cudaMemcpyHostToDevice, s));
+        if (!ctx->ptiles.empty())
+            CU(cudaMemcpyAsync(ctx->d_ptiles.p, ctx->ptiles.data(), sizeof(uint32_t) * ctx->ptiles.size(),
+                               cudaMemcpyHostToDevice, s));
         CU(cudaMemcpyAsync(ctx->d_cta_first.p, ctx->cta_first.data(),
                            sizeof(int32_t) * ctx->cta_first.size(), cudaMemcpyHostToDevice, s));
         CU(cudaStreamSynchronize(s));   // host vectors may change on the next replan
@@ -567,13 +649,20 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     //      the copy of batch k+1 overlaps the kernels of batch k ----
     FrameInfo* fi = sl.h_finfo;                    // pinned; reused only after this slot's collect
     if (!frames_on_device) {
+        // device copy: pitch and frame offsets meet the texture alignment
+        const int64_t pa = std::max<int64_t>(16, ctx->tex_pitch_align);
+        const int64_t fa = std::max<int64_t>(256, ctx->tex_align);
         std::vector<int64_t> foff(n);
         int64_t total = 0;
         for (int f = 0; f < n; ++f) {
             foff[f] = total;
-            total += round_up(round_up(frames[f].w, 16) * (int64_t)frames[f].h, 256);
+            total += round_up(round_up(frames[f].w, pa) * (int64_t)frames[f].h, fa);
         }
+        const void* old_p = sl.frames.p;
+        const size_t old_bytes = sl.frames.bytes;
         CU(sl.frames.ensure((size_t)total));
+        if (sl.frames.p != old_p && old_p)             // cudaFree above waited for all work
+            drop_textures(ctx, old_p, old_bytes);
         // the previous batch of this slot (k-2) read these frames until its end event
         if (sl.used) CU(cudaStreamWaitEvent(ctx->copy_stream, sl.ev[6], 0));
         CU(cudaEventRecord(sl.ev[0], ctx->copy_stream));
@@ -581,11 +670,11 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
         while (f < n) {
             // one 2-D copy for every run of equally-sized frames laid out back to back
             int g = f + 1;
-            const int64_t dp = round_up(frames[f].w, 16);
+            const int64_t dp = round_up(frames[f].w, pa);
             while (g < n && frames[g].w == frames[f].w && frames[g].h == frames[f].h &&
                    frames[g].pitch == frames[f].pitch &&
                    frames[g].data == frames[f].data + (int64_t)(g - f) * frames[f].h * frames[f].pitch &&
-                   dp * frames[f].h % 256 == 0)
+                   dp * frames[f].h % fa == 0)
                 ++g;
             CU(cudaMemcpy2DAsync(sl.frames.as<uint8_t>() + foff[f], dp, frames[f].data, frames[f].pitch,
                                  frames[f].w, (size_t)frames[f].h * (g - f), cudaMemcpyHostToDevice,
@@ -602,19 +691,29 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
         CU(cudaEventRecord(sl.ev[0], s));
         CU(cudaEventRecord(sl.ev[1], s));
     }
+    if (ctx->tex_cache.size() > 4096) {                // bounded cache: rebuild
+        CU(cudaStreamSynchronize(s));
+        drop_textures(ctx, nullptr, 0);
+    }
+    // texture-gather pyramid only on request: measured slower than byte gathers on B200
+    // (tld4 on 8-bit texels is TEX-throughput bound; K1)
+    bool use_tex = (ctx->debug & CCNN_DEBUG_PYR_TEX) != 0;
     for (int f = 0; f < n; ++f) {
         fi[f].level0 = ctx->frame_level0[f];
         fi[f].nlevels = ctx->frame_nlevels[f];
         fi[f].tiles = ctx->frame_tiles[f];
-        fi[f].pad = 0;
+        fi[f].tile_off = ctx->frame_tile_off[f];
+        fi[f].tex = use_tex ? frame_texture(ctx, fi[f].data, fi[f].w, fi[f].h, fi[f].pitch) : 0;
+        use_tex = use_tex && fi[f].tex != 0;
     }
     CU(cudaMemcpyAsync(sl.finfo.p, fi, sizeof(FrameInfo) * n, cudaMemcpyHostToDevice, s));
     const FrameInfo* dfi = sl.finfo.as<FrameInfo>();
     Ctrl* dctrl = sl.ctrl.as<Ctrl>();
     CU(cudaMemsetAsync(dctrl, 0, sizeof(Ctrl), s));
     CU(cudaEventRecord(sl.ev[2], s));
-    launch_pyramid(dfi, n, ctx->pyr_tiles, ctx->all_safe, ctx->arena.as<uint8_t>(),
-                   ctx->d_levels.as<LevelInfo>(), ctx->d_tabs.as<uint32_t>(), s);
+    launch_pyramid(dfi, n, ctx->pyr_tiles, ctx->all_safe, use_tex, ctx->arena.as<uint8_t>(),
+                   ctx->d_levels.as<LevelInfo>(), ctx->d_ptiles.as<uint32_t>(),
+                   ctx->d_tabs.as<uint32_t>(), s);
     CU(cudaEventRecord(sl.ev[3], s));
     launch_stage1(ctx->w1, ctx->T1, ctx->arena.as<uint8_t>(), ctx->d_levels.as<LevelInfo>(),
                   ctx->d_tasks.as<S1Task>(), ctx->d_cta_first.as<int32_t>(),

@@ -46,12 +46,12 @@ def _oracle_frames(cascade, frames, min_face, scale_step, T1, T2, Tnn, rule):
 
 
 def compare_run(det, cascade, frames, min_face, scale_step, T1, T2, Tnn, rule, check_maps=True,
-                check_levels=True):
+                check_levels=True, debug_extra=0):
     """Run the GPU detector in debug mode and the oracle on the same frames; assert parity.
     `frames`: a uint8 array (n, H, W) (ccnn_detect) or a list of 2-D frames of individual
     sizes (ccnn_detect_frames).  Returns a Report with the counts and max errors."""
     from paper_1508_01292_b200 import ccnn
-    det.set_debug(ccnn.CCNN_DEBUG_STAGE1 | ccnn.CCNN_DEBUG_LEVELS)
+    det.set_debug(ccnn.CCNN_DEBUG_STAGE1 | ccnn.CCNN_DEBUG_LEVELS | debug_extra)
     if isinstance(frames, (list, tuple)):
         frames = [np.ascontiguousarray(f, np.uint8) for f in frames]
         gboxes = det.detect_frames(frames, min_face, scale_step)

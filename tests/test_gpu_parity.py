@@ -55,13 +55,17 @@ def test_c1_parity_low_threshold(ws, cascade, rule):
     print(rep)
 
 
-def test_ragged_multi_frame_batch(ws, cascade):
-    """odd sizes, upscaled level 0 (min_face < 27), scale 1.1, several frames per call."""
+@pytest.mark.parametrize("pyr", ["tex", "ldg"])
+def test_ragged_multi_frame_batch(ws, cascade, pyr):
+    """odd sizes, upscaled level 0 (min_face < 27), scale 1.1, several frames per call; both
+    pyramid forms (texture gathers / byte gathers)."""
+    from paper_1508_01292_b200 import ccnn
     fr = synth_frames.make_stills(3, 333, 257, 991, 20)
     T1 = quantile_T1(cascade, fr, 20, 1.1, 0.995)
     T2 = (0.8, 0.1)
     det = make_det(ws, T1, T2, 1, 0)
-    rep = parity.compare_run(det, cascade, fr, 20, 1.1, T1, T2, 1, 0)
+    rep = parity.compare_run(det, cascade, fr, 20, 1.1, T1, T2, 1, 0,
+                             debug_extra=ccnn.CCNN_DEBUG_PYR_TEX if pyr == "tex" else 0)
     print(rep)
 
 
