@@ -95,17 +95,25 @@ def plant_faces(img: np.ndarray, rng: np.random.Generator, n: int, min_face: int
     return boxes
 
 
-def make_still(w: int, h: int, seed: int, min_face: int, n_faces=None,
-               clutter: bool = False) -> np.ndarray:
-    """One synthetic grayscale frame, uint8 (h, w)."""
+def make_still_gt(w: int, h: int, seed: int, min_face: int, n_faces=None,
+                  clutter: bool = False):
+    """One synthetic grayscale frame, uint8 (h, w), and its planted faces as rectangles
+    [(x, y, w, h)] (the ground truth of the NEXT #3 evaluation; clutter templates, when
+    requested, are planted too and counted as faces)."""
     rng = np.random.default_rng(seed)
     img = background(w, h, seed, clutter)
     if n_faces is None:
         n_faces = int(rng.integers(1, 6))
-    plant_faces(img, rng, n_faces, min_face, 4 * min_face)
+    gt = plant_faces(img, rng, n_faces, min_face, 4 * min_face)
     if clutter:
-        plant_faces(img, rng, 300, max(8, min_face // 2), 4 * min_face)
-    return img.astype(np.uint8)
+        gt += plant_faces(img, rng, 300, max(8, min_face // 2), 4 * min_face)
+    return img.astype(np.uint8), gt
+
+
+def make_still(w: int, h: int, seed: int, min_face: int, n_faces=None,
+               clutter: bool = False) -> np.ndarray:
+    """One synthetic grayscale frame, uint8 (h, w)."""
+    return make_still_gt(w, h, seed, min_face, n_faces, clutter)[0]
 
 
 def make_video(n: int, w: int, h: int, seed: int, min_face: int, n_faces: int = 12,

@@ -334,3 +334,25 @@ def test_mixed_size_frames_api(ws, cascade):
     rev = np.concatenate([per[len(fr) - 1 - k] for k in range(len(fr))])
     rev["frame"] = np.repeat(np.arange(len(fr)), [len(per[len(fr) - 1 - k]) for k in range(len(fr))])
     assert np.array_equal(g2, rev)
+
+
+def test_synthetic_gt_scores_match_oracle(ws, cascade):
+    """NEXT #3: FDDB / AFW protocol scores of the CUDA path's boxes on planted-face stills of
+    mixed sizes equal the scores of the oracle's boxes (evaluate.py is host-side scoring)."""
+    from paper_1508_01292_b200 import evaluate as ev
+    data = [synth_frames.make_still_gt(w, h, 500 + k, 15, n_faces=4)
+            for k, (w, h) in enumerate([(300, 260), (450, 450), (380, 290), (257, 333)])]
+    fr = [d[0] for d in data]
+    T1 = _quantile_T1_list(cascade, fr, 15, 1.05, 0.998)
+    T2 = (0.5, 0.0)
+    det = make_det(ws, T1, T2, 1, 0, max_w=512, max_h=512, max_batch=8, queue_capacity=8192)
+    g = det.detect_frames(fr, 15, 1.05)
+    _, o, _ = parity._oracle_frames(cascade, fr, 15, 1.05, T1, T2, 1, 0)
+    assert len(g) > 0
+    gp, op = ev.boxes_by_frame(g, len(fr)), ev.boxes_by_frame(o, len(fr))
+    ths = [-2.0, 0.0, 0.5]
+    # same boxes; scores within 1e-4 and none near these thresholds -> identical ROC rows
+    assert ev.score_fddb([(d[1], p[0], p[1]) for d, p in zip(data, gp)], ths) == \
+        ev.score_fddb([(d[1], p[0], p[1]) for d, p in zip(data, op)], ths)
+    assert ev.score_afw([(d[1], p[0]) for d, p in zip(data, gp)]) == \
+        ev.score_afw([(d[1], p[0]) for d, p in zip(data, op)])
