@@ -87,6 +87,7 @@ def lib():
                                      C.c_int, dp, ip, ip]
         L.or_resample.argtypes = [u8p, C.c_int, C.c_int, C.c_long, C.c_double, C.c_int, C.c_int,
                                   u8p]
+        L.or_to_gray.argtypes = [u8p, C.c_int, C.c_int, C.c_long, u8p]
         L.or_normalise.restype = C.c_double
         L.or_normalise.argtypes = [C.c_uint8]
         L.or_stage1_window.restype = C.c_double
@@ -198,6 +199,19 @@ def level_table(W, H, min_face, scale_step, max_levels=512):
     if n < 0:
         raise ValueError("bad pyramid arguments")
     return [(float(sig[k]), int(lw[k]), int(lh[k])) for k in range(n)]
+
+
+def to_gray(img):
+    """(h, w) uint8 -> itself; (h, w, 3) interleaved R,G,B -> Rec.601 luma (reading I1)."""
+    img = np.ascontiguousarray(img, np.uint8)
+    if img.ndim == 2:
+        return img.copy()
+    if img.ndim != 3 or img.shape[2] != 3:
+        raise ValueError("expected (h, w) gray or (h, w, 3) RGB")
+    h, w, _ = img.shape
+    out = np.empty((h, w), np.uint8)
+    lib().or_to_gray(_u8(img), w, h, 3 * w, _u8(out))
+    return out
 
 
 def resample(frame, sigma, lw, lh):

@@ -223,6 +223,19 @@ static uint8_t bilin_blend(int p00, int p01, int p10, int p11, int ax, int ay)
     return (uint8_t)v;
 }
 
+/* Frame ingest of an interleaved 8-bit R,G,B raster (reading I1; the paper assumes
+ * grayscale input, "original grayscale image"; SPEC S:216-223 to_grayscale):
+ * Rec.601 luma 0.299 R + 0.587 G + 0.114 B rounded to nearest, ties up -- in exact
+ * integers (299 R + 587 G + 114 B + 500) div 1000.  dst is w x h, row pitch w. */
+void or_to_gray(const uint8_t* rgb, int w, int h, long pitch, uint8_t* dst)
+{
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            const uint8_t* p = rgb + (long)y * pitch + 3L * x;
+            dst[(long)y * w + x] = (uint8_t)((299L * p[0] + 587L * p[1] + 114L * p[2] + 500L) / 1000L);
+        }
+}
+
 /* Pyramid level by bilinear resampling of the ORIGINAL frame, O2 (P:121 GPU pyramid;
  * S:228 "bilinear resampling").  dst is lw x lh, row pitch lw. */
 void or_resample(const uint8_t* src, int W, int H, long pitch, double sigma,

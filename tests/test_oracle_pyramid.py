@@ -90,3 +90,29 @@ def test_window_grid(golden):
         nx, ny = oracle.window_grid(lw, lh)
         assert nx == (lw - 27) // 4 + 1 and ny == (lh - 31) // 4 + 1
     assert oracle.window_grid(26, 40) == (0, 0)
+
+
+def test_to_gray_pins():
+    """Reading I1: gray passthrough, SPEC's examples, and exact rational
+    round-half-up of the Rec.601 luma on every tie and a random sample."""
+    from fractions import Fraction
+    g = np.arange(256, dtype=np.uint8).reshape(16, 16)
+    assert np.array_equal(oracle.to_gray(g), g)
+    px = np.array([[[255, 255, 255], [255, 0, 0], [0, 255, 0], [0, 0, 255], [0, 0, 0]]], np.uint8)
+    assert oracle.to_gray(px).tolist() == [[255, 76, 150, 29, 0]]          # round(76.245) = 76
+    # exact rational reference: floor(luma + 1/2)
+    def ref(r, gg, b):
+        v = Fraction(299, 1000) * r + Fraction(587, 1000) * gg + Fraction(114, 1000) * b
+        return int(v + Fraction(1, 2))
+    rng = np.random.default_rng(5)
+    rgb = rng.integers(0, 256, (40, 50, 3)).astype(np.uint8)
+    got = oracle.to_gray(rgb)
+    for y in range(0, 40, 3):
+        for x in range(50):
+            assert got[y, x] == ref(*map(int, rgb[y, x]))
+    # ties (luma exactly k + 1/2) round up
+    ties = [(r, gg, b) for r in range(0, 256, 5) for gg in range(0, 256, 7) for b in range(0, 256, 11)
+            if (299 * r + 587 * gg + 114 * b) % 1000 == 500][:200]
+    assert ties
+    a = np.array([ties], np.uint8)
+    assert oracle.to_gray(a)[0].tolist() == [ref(*t) for t in ties]
