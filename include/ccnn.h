@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define CCNN_ABI_VERSION 2
+#define CCNN_ABI_VERSION 3
 
 /* status codes */
 #define CCNN_OK          0
@@ -126,12 +126,17 @@ int ccnn_detect(ccnn_ctx* ctx, const uint8_t* frames, int n, int w, int h, int64
                 ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes, ccnn_stats* stats);
 
 /* One frame of a variable-size batch (stills of mixed sizes, e.g.
- * the FDDB benchmark images).  data: uint8 grayscale, w x h, row pitch `pitch`
- * bytes (>= w); host or device memory per the call's frames_on_device. */
+ * the FDDB benchmark images).  data: w x h pixels, row pitch `pitch` bytes;
+ * host or device memory per the call's frames_on_device.  channels: 0 or 1 = 8-bit
+ * grayscale (pitch >= w); 3 = interleaved 8-bit R,G,B (pitch >= 3w), converted on
+ * the GPU to Rec.601 luma (299 R + 587 G + 114 B + 500) div 1000 (reading I1, SPEC
+ * S:216-223) before the pyramid; any other value is CCNN_E_ARG.  reserved must be 0. */
 typedef struct {
     const uint8_t* data;
     int32_t w, h;
     int64_t pitch;
+    int32_t channels;
+    int32_t reserved;
 } ccnn_frame;
 
 /* ccnn_detect over n frames of individual sizes: each frame gets its own level table

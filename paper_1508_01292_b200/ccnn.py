@@ -54,7 +54,8 @@ class Box(C.Structure):
 
 
 class Frame(C.Structure):
-    _fields_ = [("data", C.c_void_p), ("w", C.c_int32), ("h", C.c_int32), ("pitch", C.c_int64)]
+    _fields_ = [("data", C.c_void_p), ("w", C.c_int32), ("h", C.c_int32), ("pitch", C.c_int64),
+                ("channels", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -223,27 +224,33 @@ class Detector:
         self._inflight.append((keep, n))
 
     def _frame_list(self, frames, stream):
-        """ccnn_frame array for a list of 2-D uint8 images (numpy arrays or torch tensors,
-        all on the host or all on the ctx device) of individual sizes."""
+        """ccnn_frame array for a list of uint8 images of individual sizes -- (h, w) gray or
+        (h, w, 3) interleaved R,G,B -- numpy arrays or torch tensors, all on the host or all
+        on the ctx device."""
         if len(frames) == 0:
             raise ValueError("empty frame list")
         keep, descs, dev = [], [], set()
         for f in frames:
             if hasattr(f, "data_ptr"):
                 import torch
-                assert f.dtype == torch.uint8 and f.dim() == 2 and f.stride(1) == 1
+                assert f.dtype == torch.uint8 and f.dim() in (2, 3)
+                ch = 1 if f.dim() == 2 else f.shape[2]
+                assert (f.stride(1) == 1) if ch == 1 else (f.stride(2) == 1 and f.stride(1) == ch)
                 if f.is_cuda and stream is None:
                     stream = torch.cuda.current_stream(f.device).cuda_stream
                 dev.add(bool(f.is_cuda))
                 keep.append(f)
-                descs.append(Frame(f.data_ptr(), f.shape[1], f.shape[0], f.stride(0)))
+                descs.append(Frame(f.data_ptr(), f.shape[1], f.shape[0], f.stride(0), ch, 0))
             else:
                 a = np.asarray(f)
-                if a.dtype != np.uint8 or a.ndim != 2 or a.strides[1] != 1:
+                ch = 1 if a.ndim == 2 else a.shape[2]
+                ok = a.dtype == np.uint8 and a.ndim in (2, 3) and \
+                    ((a.strides[1] == 1) if a.ndim == 2 else (a.strides[2] == 1 and a.strides[1] == ch))
+                if not ok:
                     a = np.ascontiguousarray(a, np.uint8)
                 dev.add(False)
                 keep.append(a)
-                descs.append(Frame(a.ctypes.data, a.shape[1], a.shape[0], a.strides[0]))
+                descs.append(Frame(a.ctypes.data, a.shape[1], a.shape[0], a.strides[0], ch, 0))
         if len(dev) != 1:
             raise ValueError("frames must be all on the host or all on the device")
         arr = (Frame * len(descs))(*descs)

@@ -6,6 +6,7 @@
 //   CNN2: C4x4 1->16, P, C3x3 16->6, P, C7x8 6->2, C1x1 2->1   (51x55 -> 5x5)
 //   CNN3: C4x4 1->2, P, C3x3 2->2, P, C7x8 2->25, C1x1 25->1   (51x55 -> 5x5)
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -47,6 +48,13 @@ struct FrameInfo {             // one frame of a batch, as the kernels read it
     int32_t tiles, tile_off;   // pyramid tiles of all its levels; their descriptors at
                                // tiles[tile_off ..] (shared by equally-sized frames)
     unsigned long long tex;    // pitch-2D uint8 texture object over data (0 = none)
+};
+struct GrayJob {               // one interleaved R,G,B frame -> its gray copy (ingest.cu)
+    const uint8_t* src;
+    int64_t src_pitch;
+    uint8_t* dst;              // 16-B aligned rows
+    int64_t dst_pitch;
+    int32_t w, h;
 };
 struct LevelInfo {             // one pyramid level of one frame of the batch
     double sigma;
@@ -119,6 +127,7 @@ constexpr int kNmsCap = 4096;  // raw boxes per frame handled by one NMS CTA
 
 // ---- launchers (stream-ordered, no sync) ----
 // pyramid: every level of every frame, from the original frames
+void launch_to_gray(const GrayJob* d_jobs, int n_jobs, int sm_count, cudaStream_t s);
 // use_tex: every frame has a texture object (FrameInfo.tex): 2x2 footprints by tex2Dgather
 void launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, bool safe,
                     bool use_tex, uint8_t* levels, const LevelInfo* d_levels,

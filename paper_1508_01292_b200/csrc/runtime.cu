@@ -99,12 +99,14 @@ struct ccnn_ctx {
     struct Slot {
         DevBuf frames;              // H2D destination (host input)
         DevBuf finfo;               // FrameInfo[n] of the batch
+        DevBuf rgb, jobs;           // host RGB staging, GrayJob[] of the batch
+        GrayJob* h_jobs = nullptr;  // pinned staging of jobs (max_batch entries)
         FrameInfo* h_finfo = nullptr;   // pinned staging of finfo (max_batch entries)
         DevBuf ctrl, out;           // control block, compacted boxes
         Ctrl* h_ctrl = nullptr;     // pinned readback of ctrl
         cudaEvent_t ev[7] = {};     // h2d0, h2d1, c0, pyramid, stage1, selective, end
         bool used = false;          // a batch has been enqueued on this slot before
-        int n = 0;
+        int n = 0, n_jobs = 0;
         uint32_t cand_cap = 0;
         int64_t windows = 0;
         bool timed = false, empty = false;
@@ -500,6 +502,7 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
         CU(cudaMallocHost(&sl.h_ctrl, sizeof(Ctrl)));
         std::memset(sl.h_ctrl, 0, sizeof(Ctrl));
         CU(cudaMallocHost(&sl.h_finfo, sizeof(FrameInfo) * (size_t)p->max_batch));
+        CU(cudaMallocHost(&sl.h_jobs, sizeof(GrayJob) * (size_t)p->max_batch));
         for (auto& e : sl.ev) CU(cudaEventCreate(&e));
         CU(sl.ctrl.ensure(sizeof(Ctrl)));
     }
@@ -541,6 +544,9 @@ void ccnn_destroy(ccnn_ctx* ctx)
         sl.frames.release();
         sl.finfo.release();
         if (sl.h_finfo) cudaFreeHost(sl.h_finfo);
+        sl.rgb.release();
+        sl.jobs.release();
+        if (sl.h_jobs) cudaFreeHost(sl.h_jobs);
         sl.ctrl.release();
         sl.out.release();
         if (sl.h_ctrl) cudaFreeHost(sl.h_ctrl);
@@ -569,7 +575,10 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
         if (!F.data) return fail(ctx, CCNN_E_ARG, "NULL frame data");
         if (F.w < 1 || F.h < 1 || F.w > ctx->max_w || F.h > ctx->max_h)
             return fail(ctx, CCNN_E_ARG, "frame size out of [1, max_w] x [1, max_h]");
-        if (F.pitch < F.w) return fail(ctx, CCNN_E_ARG, "pitch < width");
+        const int ch = F.channels == 0 ? 1 : F.channels;
+        if ((ch != 1 && ch != 3) || F.reserved != 0)
+            return fail(ctx, CCNN_E_ARG, "channels must be 0, 1 or 3 and reserved 0");
+        if (F.pitch < (int64_t)F.w * ch) return fail(ctx, CCNN_E_ARG, "pitch < width * channels");
         if ((double)kWinW / min_face * std::max(F.w, F.h) > 32000.0)
             return fail(ctx, CCNN_E_ARG, "level 0 too large (min_face too small for this frame)");
         key.dims.emplace_back(F.w, F.h);
@@ -603,6 +612,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     if (sl.empty) {
         ctx->key = key;
         sl.cand_cap = 0;
+        sl.n_jobs = 0;
         CU(cudaEventRecord(sl.ev[6], s));
         ctx->next_slot ^= 1;
         ctx->inflight++;
@@ -648,49 +658,87 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     // ---- frames: device-resident, or H2D on the copy stream (host -> device boundary);
     //      the copy of batch k+1 overlaps the kernels of batch k ----
     FrameInfo* fi = sl.h_finfo;                    // pinned; reused only after this slot's collect
-    if (!frames_on_device) {
-        // device copy: pitch and frame offsets meet the texture alignment
+    GrayJob* jobs = sl.h_jobs;
+    int n_jobs = 0;
+    {
+        // device copies (host gray frames, and every RGB frame's gray plane): pitch and frame
+        // offsets meet the texture alignment; host RGB frames are staged as they come
         const int64_t pa = std::max<int64_t>(16, ctx->tex_pitch_align);
         const int64_t fa = std::max<int64_t>(256, ctx->tex_align);
-        std::vector<int64_t> foff(n);
-        int64_t total = 0;
+        auto chans = [&](int f) { return frames[f].channels == 0 ? 1 : frames[f].channels; };
+        std::vector<int64_t> foff(n, -1), roff(n, -1);
+        int64_t total = 0, rtotal = 0;
         for (int f = 0; f < n; ++f) {
+            if (frames_on_device && chans(f) == 1) continue;      // used in place
             foff[f] = total;
             total += round_up(round_up(frames[f].w, pa) * (int64_t)frames[f].h, fa);
+            if (!frames_on_device && chans(f) == 3) {
+                roff[f] = rtotal;
+                rtotal += round_up(round_up(3LL * frames[f].w, 16) * frames[f].h, 256);
+            }
         }
-        const void* old_p = sl.frames.p;
-        const size_t old_bytes = sl.frames.bytes;
-        CU(sl.frames.ensure((size_t)total));
-        if (sl.frames.p != old_p && old_p)             // cudaFree above waited for all work
-            drop_textures(ctx, old_p, old_bytes);
-        // the previous batch of this slot (k-2) read these frames until its end event
-        if (sl.used) CU(cudaStreamWaitEvent(ctx->copy_stream, sl.ev[6], 0));
-        CU(cudaEventRecord(sl.ev[0], ctx->copy_stream));
-        int f = 0;
-        while (f < n) {
-            // one 2-D copy for every run of equally-sized frames laid out back to back
-            int g = f + 1;
+        if (total) {
+            const void* old_p = sl.frames.p;
+            const size_t old_bytes = sl.frames.bytes;
+            CU(sl.frames.ensure((size_t)total));
+            if (sl.frames.p != old_p && old_p)         // cudaFree above waited for all work
+                drop_textures(ctx, old_p, old_bytes);
+        }
+        if (rtotal) CU(sl.rgb.ensure((size_t)rtotal));
+        uint8_t* gbuf = sl.frames.as<uint8_t>();
+        for (int f = 0; f < n; ++f) {
+            if (foff[f] < 0) {
+                fi[f] = FrameInfo{frames[f].data, frames[f].pitch, frames[f].w, frames[f].h};
+                continue;
+            }
             const int64_t dp = round_up(frames[f].w, pa);
-            while (g < n && frames[g].w == frames[f].w && frames[g].h == frames[f].h &&
-                   frames[g].pitch == frames[f].pitch &&
-                   frames[g].data == frames[f].data + (int64_t)(g - f) * frames[f].h * frames[f].pitch &&
-                   dp * frames[f].h % fa == 0)
-                ++g;
-            CU(cudaMemcpy2DAsync(sl.frames.as<uint8_t>() + foff[f], dp, frames[f].data, frames[f].pitch,
-                                 frames[f].w, (size_t)frames[f].h * (g - f), cudaMemcpyHostToDevice,
-                                 ctx->copy_stream));
-            for (int q = f; q < g; ++q)
-                fi[q] = FrameInfo{sl.frames.as<uint8_t>() + foff[q], dp, frames[q].w, frames[q].h};
-            f = g;
+            fi[f] = FrameInfo{gbuf + foff[f], dp, frames[f].w, frames[f].h};
+            if (chans(f) == 3) {
+                const bool staged = !frames_on_device;
+                jobs[n_jobs++] = GrayJob{staged ? sl.rgb.as<uint8_t>() + roff[f] : frames[f].data,
+                                         staged ? round_up(3LL * frames[f].w, 16) : frames[f].pitch,
+                                         gbuf + foff[f], dp, frames[f].w, frames[f].h};
+            }
         }
-        CU(cudaEventRecord(sl.ev[1], ctx->copy_stream));
-        CU(cudaStreamWaitEvent(s, sl.ev[1], 0));
-    } else {
-        for (int f = 0; f < n; ++f)
-            fi[f] = FrameInfo{frames[f].data, frames[f].pitch, frames[f].w, frames[f].h};
-        CU(cudaEventRecord(sl.ev[0], s));
-        CU(cudaEventRecord(sl.ev[1], s));
+        cudaStream_t cs = frames_on_device ? s : ctx->copy_stream;
+        if (!frames_on_device) {
+            // the previous batch of this slot (k-2) read these buffers until its end event
+            if (sl.used) CU(cudaStreamWaitEvent(ctx->copy_stream, sl.ev[6], 0));
+        }
+        CU(cudaEventRecord(sl.ev[0], cs));
+        if (!frames_on_device) {
+            int f = 0;
+            while (f < n) {
+                if (chans(f) == 3) {                   // host RGB -> staging
+                    CU(cudaMemcpy2DAsync(sl.rgb.as<uint8_t>() + roff[f], round_up(3LL * frames[f].w, 16),
+                                         frames[f].data, frames[f].pitch, 3 * (size_t)frames[f].w,
+                                         frames[f].h, cudaMemcpyHostToDevice, cs));
+                    ++f;
+                    continue;
+                }
+                // one 2-D copy for every run of equally-sized gray frames laid out back to back
+                int g = f + 1;
+                const int64_t dp = round_up(frames[f].w, pa);
+                while (g < n && chans(g) == 1 && frames[g].w == frames[f].w &&
+                       frames[g].h == frames[f].h && frames[g].pitch == frames[f].pitch &&
+                       frames[g].data == frames[f].data + (int64_t)(g - f) * frames[f].h * frames[f].pitch &&
+                       foff[g] == foff[f] + (int64_t)(g - f) * dp * frames[f].h)
+                    ++g;
+                CU(cudaMemcpy2DAsync(gbuf + foff[f], dp, frames[f].data, frames[f].pitch, frames[f].w,
+                                     (size_t)frames[f].h * (g - f), cudaMemcpyHostToDevice, cs));
+                f = g;
+            }
+        }
+        if (n_jobs) {
+            CU(sl.jobs.ensure(sizeof(GrayJob) * n_jobs));
+            CU(cudaMemcpyAsync(sl.jobs.p, jobs, sizeof(GrayJob) * n_jobs, cudaMemcpyHostToDevice, cs));
+            launch_to_gray(sl.jobs.as<GrayJob>(), n_jobs, ctx->sm_count, cs);
+            CU(cudaGetLastError());
+        }
+        CU(cudaEventRecord(sl.ev[1], cs));
+        if (!frames_on_device) CU(cudaStreamWaitEvent(s, sl.ev[1], 0));
     }
+    sl.n_jobs = n_jobs;
     if (ctx->tex_cache.size() > 4096) {                // bounded cache: rebuild
         CU(cudaStreamSynchronize(s));
         drop_textures(ctx, nullptr, 0);
@@ -784,7 +832,7 @@ int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_box
         stats->stage2 = hc.n_stage2;
         stats->stage3 = hc.n_stage3;
         stats->nms = hc.n_out;
-        stats->kernel_launches = 4;
+        stats->kernel_launches = 4 + (sl.n_jobs ? 1 : 0);
         const int from[5] = {0, 2, 3, 4, 5}, to[5] = {1, 3, 4, 5, 6};
         for (int k = 0; k < 5; ++k) {
             float t = 0.f;

@@ -42,7 +42,7 @@ def test_exports_every_declared_symbol(lib):
     assert declared <= exported, declared - exported
     for name in declared:
         getattr(lib, name)
-    assert lib.ccnn_abi_version() == 2
+    assert lib.ccnn_abi_version() == 3
 
 
 def test_sm100a_code_present():
@@ -59,9 +59,9 @@ def test_struct_layouts_match_header(tmp_path):
 int main(void){
  printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(ccnn_layer), sizeof(ccnn_net), sizeof(ccnn_params),
         sizeof(ccnn_box), sizeof(ccnn_stats), sizeof(ccnn_candidate), sizeof(ccnn_frame));
- printf("%zu %zu %zu %zu %zu %zu\\n", offsetof(ccnn_params, T1), offsetof(ccnn_params, Tnn),
+ printf("%zu %zu %zu %zu %zu %zu %zu\\n", offsetof(ccnn_params, T1), offsetof(ccnn_params, Tnn),
         offsetof(ccnn_params, segment_rows), offsetof(ccnn_stats, ms), offsetof(ccnn_candidate, r3),
-        offsetof(ccnn_frame, pitch));
+        offsetof(ccnn_frame, pitch), offsetof(ccnn_frame, channels));
  return 0;}
 """)
     exe = tmp_path / "sizes"
@@ -73,7 +73,8 @@ int main(void){
                      C.sizeof(ccnn.Box), C.sizeof(ccnn.Stats), C.sizeof(ccnn.Candidate),
                      C.sizeof(ccnn.Frame)]
     assert offs == [ccnn.Params.T1.offset, ccnn.Params.Tnn.offset, ccnn.Params.segment_rows.offset,
-                    ccnn.Stats.ms.offset, ccnn.Candidate.r3.offset, ccnn.Frame.pitch.offset]
+                    ccnn.Stats.ms.offset, ccnn.Candidate.r3.offset, ccnn.Frame.pitch.offset,
+                    ccnn.Frame.channels.offset]
     assert ccnn.BOX_DTYPE.itemsize == C.sizeof(ccnn.Box)
     assert ccnn.CAND_DTYPE.itemsize == C.sizeof(ccnn.Candidate)
 

@@ -356,3 +356,49 @@ def test_synthetic_gt_scores_match_oracle(ws, cascade):
         ev.score_fddb([(d[1], p[0], p[1]) for d, p in zip(data, op)], ths)
     assert ev.score_afw([(d[1], p[0]) for d, p in zip(data, gp)]) == \
         ev.score_afw([(d[1], p[0]) for d, p in zip(data, op)])
+
+
+def test_rgb_ingest(ws, cascade):
+    """Interleaved R,G,B frames (host, pinned, device, pitched device; mixed with gray frames
+    in one batch) give exactly the boxes and pyramid levels of their oracle Rec.601 gray
+    planes (reading I1)."""
+    import torch
+    from paper_1508_01292_b200 import ccnn
+    rng = np.random.default_rng(21)
+    grays = [synth_frames.make_still(w, h, 300 + k, 20) for k, (w, h) in
+             enumerate([(333, 257), (320, 240), (201, 150)])]
+    # colourise: R,G,B planes that are not a function of the gray value alone
+    rgbs = [np.stack([g, np.clip(g.astype(int) + rng.integers(-40, 41, g.shape), 0, 255),
+                      rng.integers(0, 256, g.shape)], 2).astype(np.uint8) for g in grays]
+    ref_gray = [oracle.to_gray(x) for x in rgbs]
+    mixed = [rgbs[0], grays[1], rgbs[2]]
+    mixed_gray = [ref_gray[0], grays[1], ref_gray[2]]
+    T1 = _quantile_T1_list(cascade, mixed_gray, 20, 1.15, 0.995)
+    det = make_det(ws, T1, (0.8, 0.1), 1, 0, max_w=640, max_h=480, max_batch=8)
+    ref = det.detect_frames(mixed_gray, 20, 1.15)
+    det.set_debug(ccnn.CCNN_DEBUG_LEVELS)
+    got = det.detect_frames(mixed, 20, 1.15)
+    assert np.array_equal(got, ref)
+    assert det.last_stats["kernel_launches"] == 5
+    for f in (0, 2):
+        for l, (s, lw, lh) in enumerate(oracle.level_table(mixed[f].shape[1], mixed[f].shape[0], 20, 1.15)[:3]):
+            assert np.array_equal(det.level_image(f, l), oracle.resample(mixed_gray[f], s, lw, lh))
+    pinned = [torch.from_numpy(x).pin_memory() for x in mixed]
+    assert np.array_equal(det.detect_frames(pinned, 20, 1.15), ref)
+    dev = [torch.from_numpy(x).cuda() for x in mixed]
+    assert np.array_equal(det.detect_frames(dev, 20, 1.15), ref)
+    pitched = []
+    for x in mixed:                                     # odd row pitch on the device
+        big = torch.zeros((x.shape[0], x.shape[1] + 7) + x.shape[2:], dtype=torch.uint8, device="cuda")
+        big[:, :x.shape[1]] = torch.from_numpy(x).cuda()
+        pitched.append(big[:, :x.shape[1]])
+    assert np.array_equal(det.detect_frames(pitched, 20, 1.15), ref)
+    # streaming with RGB
+    det.submit_frames(pinned, 20, 1.15)
+    det.submit_frames(dev, 20, 1.15)
+    assert np.array_equal(det.collect(), ref)
+    assert np.array_equal(det.collect(), ref)
+    # bad channel counts are argument errors
+    with pytest.raises(ccnn.CcnnError) as e:
+        det.detect_frames([np.zeros((40, 40, 2), np.uint8)], 20, 1.15)
+    assert e.value.code == ccnn.CCNN_E_ARG
