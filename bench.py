@@ -309,7 +309,9 @@ def main():
             "roofline": {"bound": "alu", "achieved": achieved_tflops, "peak": fp32_peak,
                          "unit": "TFLOP/s", "frac": achieved_tflops / fp32_peak, "traffic": traffic,
                          "kernel": "stage1_kernel",
-                         "peak_note": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)"},
+                         "peak_note": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json); "
+                                      "achieved = algorithmic fp32 FLOPs (layers 2-4 on FFMA, layer 1 as "
+                                      "fp16 hi+lo mma.sync, DESIGN.md K2)"},
             "e2e": {"value": world * batch * e2e_steps / (ms_e2e / 1000.0), "unit": "frames/s",
                     "h2d_bytes_per_step": int(frames.nbytes), "d2h_bytes_per_step": int(d2h // e2e_steps)},
             "gpu_launches": int(launches),

@@ -26,6 +26,13 @@ struct __align__(16) Cnn1W {   // 797 weights + re-arranged copies for the stage
     float w2[6][6][9], b2[6];  // [out][in][ky*3+kx]
     float w3[2][6][30], b3[2]; // [out][in][ky*5+kx]
     float w4[2], b4;
+    // layer 1 on the tensor cores (stage1.cu, S1_HMMA): per lane the mma.m16n8k16 B fragments
+    // of W' = w1 / 127.5 * 2^s (raw pixel inputs, the O3 normalisation folded in) split into
+    // fp16 hi + lo parts, [hi/lo][lane][reg] (maps 6, 7 zero); b1h = b1 - sum_k w1; the
+    // accumulator is scaled back by l1_inv_scale = 2^-s
+    uint32_t l1frag[2][32][2];
+    float b1h[8];
+    float l1_inv_scale;
 };
 template <int A, int B, int C>
 struct __align__(16) SelNetW { // CNN2: <16,6,2>, CNN3: <2,2,25>

@@ -18,6 +18,7 @@
 
 #include "../../include/ccnn.h"
 #include "ccnn_internal.h"
+#include <cuda_fp16.h>
 
 using namespace ccnn;
 
@@ -171,6 +172,8 @@ int64_t conv_params(const int (*ref)[5], int nl)
 
 // The weight blob is [kernels][bias] per conv layer (S:186 order); our structs hold the
 // same values in the same order, so a straight copy per layer suffices.
+inline float o_w1(int o, int k, const float* w) { return w[o * 16 + k]; }   // layer-1 [out][tap]
+
 void unpack_cnn1(const float* w, Cnn1W& o)
 {
     const float* p = w;
@@ -182,6 +185,38 @@ void unpack_cnn1(const float* w, Cnn1W& o)
     std::memcpy(o.b3, p, sizeof(o.b3)); p += 2;
     std::memcpy(o.w4, p, sizeof(o.w4)); p += 2;
     o.b4 = *p;
+    {                                                // tensor-core layer-1 fragments
+        double mx = 0.0;
+        for (int o = 0; o < 6; ++o)
+            for (int k = 0; k < 16; ++k) mx = std::max(mx, std::fabs((double)o_w1(o, k, w)) / 127.5);
+        // scale so that max |W'| lies in [8, 16): fp16 hi/lo parts stay normal
+        const int e = mx > 0.0 ? (int)std::floor(std::log2(mx)) : 0;
+        const double sc = std::ldexp(1.0, 3 - e);
+        o.l1_inv_scale = (float)std::ldexp(1.0, e - 3);
+        auto part = [&](int o_, int k, int lo) -> uint16_t {
+            if (o_ >= 6) return 0;
+            const float wp = (float)((double)o_w1(o_, k, w) / 127.5 * sc);
+            const __half hi = __float2half_rn(wp);
+            if (!lo) return __half_as_ushort(hi);
+            return __half_as_ushort(__float2half_rn(wp - __half2float(hi)));
+        };
+        for (int lo = 0; lo < 2; ++lo)
+            for (int lane = 0; lane < 32; ++lane) {
+                const int n = lane / 4, k0 = (lane % 4) * 2;
+                for (int r = 0; r < 2; ++r) {
+                    const int k = k0 + 8 * r;
+                    o.l1frag[lo][lane][r] = (uint32_t)part(n, k, lo) | ((uint32_t)part(n, k + 1, lo) << 16);
+                }
+            }
+        for (int m = 0; m < 8; ++m) {
+            double b = 0.0;
+            if (m < 6) {
+                b = (double)o.b1[m];
+                for (int k = 0; k < 16; ++k) b -= (double)o_w1(m, k, w);
+            }
+            o.b1h[m] = (float)b;
+        }
+    }
     for (int ci = 0; ci < 6; ++ci) {                 // vector-friendly copies (stage1.cu)
         for (int k = 0; k < 56; ++k) o.w2v[ci][k] = k < 54 ? o.w2[k / 9][ci][k % 9] : 0.f;
         for (int i = 0; i < 6; ++i)

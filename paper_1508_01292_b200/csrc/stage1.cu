@@ -48,6 +48,16 @@ __device__ __forceinline__ float act(float x)
 #define S1_MIN_BLOCKS 5
 #endif
 
+#ifndef S1_HMMA
+#define S1_HMMA 1                       // layer 1 on the tensor cores (mma.sync m16n8k16)
+#endif
+#ifndef S1_L2_UNROLL
+#define S1_L2_UNROLL 1                  // layer-2 input-map loop unrolled
+#endif
+#ifndef S1_L3_UNROLL
+#define S1_L3_UNROLL 0
+#endif
+
 constexpr int NT = 128;                 // threads per CTA
 constexpr int TW = NT / 2 - 5;          // 59 windows per band
 constexpr int IN_WORDS = NT / 2 + 1;    // 65 32-bit words cover the 4*TW+23 = 259 input columns
@@ -59,7 +69,13 @@ constexpr int P1_RS = NT + 20;          // one (row, map) of the P1 ring (+4: L2
 constexpr int P1_RING = 6;              // rows 4v-2 .. 4v+3
 constexpr int P2_RS = NT / 2 + 8;
 constexpr int P2_RING = 4;              // rows 2v-3 .. 2v
-constexpr int SMEM_FLOATS = IN_RING * IN_RS + P1_RING * 6 * P1_RS + P2_RING * 6 * P2_RS;
+// S1_HMMA input ring: raw pixels as fp16 pairs, two copies per row -- copy0 word j = pixels
+// (2j, 2j+1), copy1 word j = pixels (2j+1, 2j+2) -- so every A-fragment pair is one aligned
+// 32-bit load; row stride 272 words (== 16 mod 32: rows y, y+1 of one load hit disjoint banks)
+constexpr int IN_CW = 136;              // words per copy (130 used)
+constexpr int IN_RSW = 2 * IN_CW;       // words per ring row
+constexpr int IN_FLOATS = S1_HMMA ? IN_RING * IN_RSW : IN_RING * IN_RS;
+constexpr int SMEM_FLOATS = IN_FLOATS + P1_RING * 6 * P1_RS + P2_RING * 6 * P2_RS;
 // loader: 8 new input rows x 65 words per super-step = 520 loads on 128 threads.  Thread t
 // owns ONE word column (t < 65: word t of rows 0-3; else word t-65 of rows 4-7) plus, for
 // t < 8, one leftover (word 63 + (t&1) of row 4 + (t>>1)) -- so a thread's loads come from
@@ -71,6 +87,7 @@ __device__ __forceinline__ float u8f(uint32_t v)
     return fmaf((float)v, 1.0f / 127.5f, -1.0f);   // O3: (v - 127.5) / 127.5
 }
 
+#if !S1_HMMA
 __device__ __forceinline__ void store_word(float* ring, int slot, int w, uint32_t word)
 {
     float* row = ring + slot * IN_RS;
@@ -79,6 +96,39 @@ __device__ __forceinline__ void store_word(float* ring, int slot, int w, uint32_
     *reinterpret_cast<float2*>(row + 2 * w) = ev;
     *reinterpret_cast<float2*>(row + IN_ODD + 2 * w) = od;
 }
+#else
+// two bytes of `word` (selector) -> an fp16 pair of the exact pixel values: 0x64pp is the
+// fp16 1024 + p, minus 1024
+__device__ __forceinline__ uint32_t h2_of(uint32_t word, uint32_t sel)
+{
+    const uint32_t t = __byte_perm(word, 0x64646464u, sel);
+    uint32_t r;
+    asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(t), "r"(0x64006400u));
+    return r;
+}
+// input word w (pixels 4w .. 4w+3) of ring row `slot`: copy0 words 2w, 2w+1; copy1 word 2w
+// and the halves 4w-1 (upper half of word 2w-1) and 4w+2 (lower half of word 2w+1)
+__device__ __forceinline__ void store_word(float* ring, int slot, int w, uint32_t word)
+{
+    uint32_t* row = reinterpret_cast<uint32_t*>(ring) + slot * IN_RSW;
+    *reinterpret_cast<uint2*>(row + 2 * w) = make_uint2(h2_of(word, 0x4140), h2_of(word, 0x4342));
+    uint32_t* c1 = row + IN_CW;
+    const uint32_t mid = h2_of(word, 0x4241);                  // pixels (4w+1, 4w+2)
+    const uint32_t edge = h2_of(word, 0x4340);                 // pixels (4w, 4w+3)
+    c1[2 * w] = mid;
+    uint16_t* c1h = reinterpret_cast<uint16_t*>(c1);
+    if (w > 0) c1h[4 * w - 1] = (uint16_t)(edge & 0xFFFFu);
+    c1h[4 * w + 2] = (uint16_t)(edge >> 16);
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1)
+{
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+#endif
 
 __device__ __forceinline__ int pmod(int a, int m) { return ((a % m) + m) % m; }
 
@@ -92,7 +142,7 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
 {
     extern __shared__ __align__(16) float smem[];
     float* const in_ring = smem;
-    float* const p1_ring = in_ring + IN_RING * IN_RS;
+    float* const p1_ring = in_ring + IN_FLOATS;
     float* const p2_ring = p1_ring + P1_RING * 6 * P1_RS;
 
     const int tid = threadIdx.x;
@@ -105,6 +155,14 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
     const int j3 = 16 * warp + (lane >> 1);
     const int r3 = lane & 1;
 
+#if S1_HMMA
+    // layer-1 MMA fragments: lane = (group m, thread-in-group c4); B (weights, hi / lo) and
+    // the bias of this lane's two maps stay in registers for the whole kernel
+    const int c4 = lane & 3, mg = lane >> 2;
+    const uint32_t bh0 = W.l1frag[0][lane][0], bh1 = W.l1frag[0][lane][1];
+    const uint32_t bl0 = W.l1frag[1][lane][0], bl1 = W.l1frag[1][lane][1];
+    const float bias0 = W.b1h[2 * c4], bias1 = W.b1h[2 * c4 + 1];
+#endif
     const int ld_w = tid < IN_WORDS ? tid : tid - IN_WORDS;      // primary word column
     const int ld_r0 = tid < IN_WORDS ? 0 : 4;                      // its rows ld_r0 .. +3
     const bool ld_x = tid < 8;                                     // leftover load
@@ -174,6 +232,52 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
         for (int v = 0; v < nsteps; ++v) {
             // ---- L1: conv4x4 1->6, pool, act -> P1 rows 4v .. 4v+3 (input rows 8v .. 8v+10);
             //      thread = P1 column, two row pairs ----
+#if S1_HMMA
+            // tensor-core form: a tile = 16 conv-1 outputs of one conv row (rows m / m+8 of the
+            // MMA = columns xb+2m / xb+2m+1), K = the 16 taps, N = 8 maps (6 used); the tile
+            // pair (conv rows 2p, 2p+1) holds whole 2x2 pool cells in each thread
+#pragma unroll 1
+            for (int pr = 0; pr < 4; ++pr) {
+                const uint32_t* const ring32 = reinterpret_cast<const uint32_t*>(in_ring);
+                int sl[5];
+#pragma unroll
+                for (int q = 0; q < 5; ++q) {
+                    int t = (8 * v + 2 * pr + (c4 >> 1) + q) % IN_RING;
+                    sl[q] = t * IN_RSW;
+                }
+                const int p1slot = (4 * v + pr) % P1_RING;
+                // all four tile pairs' MMAs first, then their epilogues: the MMA latency of
+                // one pair is covered by the others
+                float dA[4][4], dB[4][4];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const int xw = 8 * (4 * warp + g) + mg + (c4 & 1);     // word of pixel xb+2m+kx0
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) { dA[g][k] = 0.f; dB[g][k] = 0.f; }
+                    const uint32_t a0 = ring32[sl[0] + xw], a1 = ring32[sl[0] + IN_CW + xw];
+                    const uint32_t a2 = ring32[sl[2] + xw], a3 = ring32[sl[2] + IN_CW + xw];
+                    const uint32_t e0 = ring32[sl[1] + xw], e1 = ring32[sl[1] + IN_CW + xw];
+                    const uint32_t e2 = ring32[sl[3] + xw], e3 = ring32[sl[3] + IN_CW + xw];
+                    mma16816(dA[g], a0, a1, a2, a3, bh0, bh1);
+                    mma16816(dB[g], e0, e1, e2, e3, bh0, bh1);
+                    mma16816(dA[g], a0, a1, a2, a3, bl0, bl1);
+                    mma16816(dB[g], e0, e1, e2, e3, bl0, bl1);
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const float m0 = fmaxf(fmaxf(dA[g][0], dA[g][2]), fmaxf(dB[g][0], dB[g][2]));
+                    const float m1 = fmaxf(fmaxf(dA[g][1], dA[g][3]), fmaxf(dB[g][1], dB[g][3]));
+                    const int col = 8 * (4 * warp + g) + mg;                // P1 column
+                    const int pcol = (col & 1) ? P1_ODD + (col >> 1) : (col >> 1);
+                    const float v0 = act(fmaf(m0, W.l1_inv_scale, bias0));
+                    const float v1 = act(fmaf(m1, W.l1_inv_scale, bias1));
+                    if (c4 < 3) {
+                        p1_ring[(p1slot * 6 + 2 * c4) * P1_RS + pcol] = v0;
+                        p1_ring[(p1slot * 6 + 2 * c4 + 1) * P1_RS + pcol] = v1;
+                    }
+                }
+            }
+#else
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
                 const int c = tid;
@@ -215,6 +319,7 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
                             act(fmaxf(fmaxf(a[0][o], a[1][o]), fmaxf(a[2][o], a[3][o])));
                 }
             }
+#endif
 
             __syncthreads();   // P1 rows 4v..4v+3 visible; input rows 8v..8v+7 dead
 
@@ -239,7 +344,11 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
                 for (int o = 0; o < 6; ++o)
 #pragma unroll
                     for (int k = 0; k < 4; ++k) a[o][k] = W.b2[o];
+#if S1_L2_UNROLL
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
                 for (int ci = 0; ci < 6; ++ci) {
                     float xv[4][4];
 #pragma unroll
@@ -282,7 +391,11 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
             {
                 const int p = 2 * v - 3 + r3;
                 const float* p2 = p2_ring + pmod(p, P2_RING) * 6 * P2_RS;
+#if S1_L3_UNROLL
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
                 for (int ci = 0; ci < 6; ++ci) {
                     float xv[5];
 #pragma unroll
