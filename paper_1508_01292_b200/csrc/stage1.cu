@@ -15,12 +15,16 @@
 //    so no per-level launches (the paper's small-level launch overhead);
 //  * line-buffer pipeline in shared memory marching down the band, TWO window rows per
 //    "super-step", two __syncthreads per super-step (layer 1 | loader + layers 2, 3):
-//    input ring (fp32, even/odd de-interleaved columns -> conflict-free LDS), pooled-
-//    layer-1 ring, pooled-layer-2 ring, 40 KB in all -> 5 CTAs per SM;
-//  * work is split over DATA only (columns x rows), never over maps or taps, so all 128
-//    threads run one instruction stream whose weights are warp-uniform: every MAC is an
-//    FFMA with a uniform-register (constant-bank kernel parameter) operand, rolled loops
-//    index the constant bank with uniform counters (LDCU [UR+imm]);
+//    input ring, pooled-layer-1 ring, pooled-layer-2 ring, 41 KB in all -> 5 CTAs per SM;
+//  * layer 1 (half the FLOPs) on the tensor cores: mma.sync m16n8k16, A = 16 conv outputs
+//    x 16 taps of raw pixels (exact in fp16; the input ring holds fp16 pairs in two copies
+//    shifted by one pixel so every fragment pair is an aligned 32-bit load), B = the six
+//    maps' weights / 127.5 * 2^s split into fp16 hi + lo parts (two MMAs, fp32 accumulate:
+//    ~2^-22 relative weight error), bias and 2^-s applied after the pooling max;
+//    S1_HMMA=0 builds the all-FFMA form;
+//  * layers 2-4: work is split over DATA only (columns x rows), never over maps or taps, so
+//    all 128 threads run one instruction stream whose weights are warp-uniform: every MAC is
+//    an FFMA with a uniform-register (constant-bank kernel parameter) operand;
 //  * max-pool BEFORE the activation (Eq. 1 is monotone: act(max) == max(act));
 //    layer 3 streams P2 rows through register accumulators, the even/odd rows of a pair
 //    on adjacent lanes, partial sums combined with one shfl per output;
