@@ -69,7 +69,8 @@ constexpr int IN_ODD = NT + 4;          // odd input columns start inside a ring
 constexpr int IN_RS = 2 * NT + 8;       // input ring row stride (floats)
 constexpr int IN_RING = 12;             // rows 8v .. 8v+10 (+ 8v+11 .. 8v+18 after the mid barrier)
 constexpr int P1_ODD = NT / 2 + 16;     // odd P1 columns start (bank offset 16)
-constexpr int P1_RS = NT + 20;          // one (row, map) of the P1 ring (+4: L2 lane 63 reads [144])
+constexpr int P1_RS = NT + 18;          // one (row, map) of the P1 ring (L2 lane 63 reads [144]);
+                                        // == 2 mod 16: layer-1 stores of maps 0/2/4 x even/odd hit disjoint banks
 constexpr int P1_RING = 6;              // rows 4v-2 .. 4v+3
 constexpr int P2_RS = NT / 2 + 8;
 constexpr int P2_RING = 4;              // rows 2v-3 .. 2v
@@ -79,7 +80,8 @@ constexpr int P2_RING = 4;              // rows 2v-3 .. 2v
 constexpr int IN_CW = 136;              // words per copy (130 used)
 constexpr int IN_RSW = 2 * IN_CW;       // words per ring row
 constexpr int IN_FLOATS = S1_HMMA ? IN_RING * IN_RSW : IN_RING * IN_RS;
-constexpr int SMEM_FLOATS = IN_FLOATS + P1_RING * 6 * P1_RS + P2_RING * 6 * P2_RS;
+constexpr int P1_SCRATCH = S1_HMMA ? P1_RS + 16 : 0;   // sink of the zero maps' stores
+constexpr int SMEM_FLOATS = IN_FLOATS + P1_RING * 6 * P1_RS + P2_RING * 6 * P2_RS + P1_SCRATCH;
 // loader: 8 new input rows x 65 words per super-step = 520 loads on 128 threads.  Thread t
 // owns ONE word column (t < 65: word t of rows 0-3; else word t-65 of rows 4-7) plus, for
 // t < 8, one leftover (word 63 + (t&1) of row 4 + (t>>1)) -- so a thread's loads come from
@@ -166,6 +168,12 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
     const uint32_t bh0 = W.l1frag[0][lane][0], bh1 = W.l1frag[0][lane][1];
     const uint32_t bl0 = W.l1frag[1][lane][0], bl1 = W.l1frag[1][lane][1];
     const float bias0 = W.b1h[2 * c4], bias1 = W.b1h[2 * c4 + 1];
+    // P1 column of tile pair g: 32 * warp + 8 * g + mg (even / odd columns de-interleaved:
+    // + 4 g in the store index); the lane's first map row 2 * c4
+    const int p1_col0 = 32 * warp + mg;
+    const int p1_lane = 2 * c4 * P1_RS + ((mg & 1) ? P1_ODD + (p1_col0 >> 1) : (p1_col0 >> 1));
+    const int xw0 = 32 * warp + mg + (c4 & 1);                    // input word, tile pair 0
+    float* const p1_scratch = p2_ring + P2_RING * 6 * P2_RS;
 #endif
     const int ld_w = tid < IN_WORDS ? tid : tid - IN_WORDS;      // primary word column
     const int ld_r0 = tid < IN_WORDS ? 0 : 4;                      // its rows ld_r0 .. +3
@@ -240,22 +248,27 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
             // tensor-core form: a tile = 16 conv-1 outputs of one conv row (rows m / m+8 of the
             // MMA = columns xb+2m / xb+2m+1), K = the 16 taps, N = 8 maps (6 used); the tile
             // pair (conv rows 2p, 2p+1) holds whole 2x2 pool cells in each thread
+            {
+            const uint32_t* const ring32 = reinterpret_cast<const uint32_t*>(in_ring);
+            const int rbase = (8 * v) % IN_RING + (c4 >> 1);          // ring row of input row 8v+ky0
 #pragma unroll 1
             for (int pr = 0; pr < 4; ++pr) {
-                const uint32_t* const ring32 = reinterpret_cast<const uint32_t*>(in_ring);
-                int sl[5];
+                int sl[4];
 #pragma unroll
-                for (int q = 0; q < 5; ++q) {
-                    int t = (8 * v + 2 * pr + (c4 >> 1) + q) % IN_RING;
-                    sl[q] = t * IN_RSW;
+                for (int q = 0; q < 4; ++q) {
+                    const int t = rbase + 2 * pr + q;                 // < 2 * IN_RING
+                    sl[q] = (t >= IN_RING ? t - IN_RING : t) * IN_RSW;
                 }
+                // this lane's two maps of P1 row 4v+pr (lanes c4 = 3 hold the zero maps 6, 7:
+                // their stores go to a scratch area instead of a branch)
                 const int p1slot = (4 * v + pr) % P1_RING;
+                float* const p1dst = (c4 < 3) ? p1_ring + p1slot * 6 * P1_RS + p1_lane : p1_scratch;
                 // all four tile pairs' MMAs first, then their epilogues: the MMA latency of
                 // one pair is covered by the others
                 float dA[4][4], dB[4][4];
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
-                    const int xw = 8 * (4 * warp + g) + mg + (c4 & 1);     // word of pixel xb+2m+kx0
+                    const int xw = xw0 + 8 * g;                          // word of pixel xb+2m+kx0
 #pragma unroll
                     for (int k = 0; k < 4; ++k) { dA[g][k] = 0.f; dB[g][k] = 0.f; }
                     const uint32_t a0 = ring32[sl[0] + xw], a1 = ring32[sl[0] + IN_CW + xw];
@@ -271,15 +284,10 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
                 for (int g = 0; g < 4; ++g) {
                     const float m0 = fmaxf(fmaxf(dA[g][0], dA[g][2]), fmaxf(dB[g][0], dB[g][2]));
                     const float m1 = fmaxf(fmaxf(dA[g][1], dA[g][3]), fmaxf(dB[g][1], dB[g][3]));
-                    const int col = 8 * (4 * warp + g) + mg;                // P1 column
-                    const int pcol = (col & 1) ? P1_ODD + (col >> 1) : (col >> 1);
-                    const float v0 = act(fmaf(m0, W.l1_inv_scale, bias0));
-                    const float v1 = act(fmaf(m1, W.l1_inv_scale, bias1));
-                    if (c4 < 3) {
-                        p1_ring[(p1slot * 6 + 2 * c4) * P1_RS + pcol] = v0;
-                        p1_ring[(p1slot * 6 + 2 * c4 + 1) * P1_RS + pcol] = v1;
-                    }
+                    p1dst[4 * g] = act(fmaf(m0, W.l1_inv_scale, bias0));          // P1 column +8g
+                    p1dst[4 * g + P1_RS] = act(fmaf(m1, W.l1_inv_scale, bias1));
                 }
+            }
             }
 #else
 #pragma unroll 1

@@ -9,7 +9,7 @@ ins = [(int(r[col["Address"]], 16) - base, r[col["Source"]].strip(), r) for r in
 reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 loops = []
 for i, (a, t, _) in enumerate(ins):
-    m = re.search(r"BRA\s+.*?0x([0-9a-f]+)", t)
+    m = re.search(r"BRA(?:\.U)?\s+.*?0x([0-9a-f]+)", t)
     if m:
         ta = int(m.group(1), 16) - base
         if ta < a:

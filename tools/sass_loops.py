@@ -1,7 +1,7 @@
-"""Instruction mix per loop (backward-branch region) of /tmp/mix.sass (tools/sass_mix.sh)."""
+"""Instruction mix per loop (backward-branch region) of build_tools/mix.sass (tools/sass_mix.sh)."""
 import re, collections
 ins = []
-for l in open('/tmp/mix.sass'):
+for l in open('build_tools/mix.sass'):
     m = re.match(r'\s+/\*([0-9a-f]+)\*/\s+(.*?);', l)
     if m: ins.append((int(m.group(1), 16), m.group(2).strip()))
 loops = []
