@@ -80,8 +80,7 @@ constexpr int P2_RING = 4;              // rows 2v-3 .. 2v
 constexpr int IN_CW = 136;              // words per copy (130 used)
 constexpr int IN_RSW = 2 * IN_CW;       // words per ring row
 constexpr int IN_FLOATS = S1_HMMA ? IN_RING * IN_RSW : IN_RING * IN_RS;
-constexpr int P1_SCRATCH = S1_HMMA ? P1_RS + 16 : 0;   // sink of the zero maps' stores
-constexpr int SMEM_FLOATS = IN_FLOATS + P1_RING * 6 * P1_RS + P2_RING * 6 * P2_RS + P1_SCRATCH;
+constexpr int SMEM_FLOATS = IN_FLOATS + P1_RING * 6 * P1_RS + P2_RING * 6 * P2_RS;
 // loader: 8 new input rows x 65 words per super-step = 520 loads on 128 threads.  Thread t
 // owns ONE word column (t < 65: word t of rows 0-3; else word t-65 of rows 4-7) plus, for
 // t < 8, one leftover (word 63 + (t&1) of row 4 + (t>>1)) -- so a thread's loads come from
@@ -125,6 +124,14 @@ __device__ __forceinline__ void store_word(float* ring, int slot, int w, uint32_
     uint16_t* c1h = reinterpret_cast<uint16_t*>(c1);
     if (w > 0) c1h[4 * w - 1] = (uint16_t)(edge & 0xFFFFu);
     c1h[4 * w + 2] = (uint16_t)(edge >> 16);
+}
+
+// P1 stores of a lane's two maps (rows 2c4, 2c4+1), skipped for the zero maps (c4 == 3)
+__device__ __forceinline__ void st2_pred(uint32_t saddr, float v0, float v1, int c4)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %3, 3;\n\t"
+                 "@p st.shared.f32 [%0], %1;\n\t@p st.shared.f32 [%0+%4], %2;\n\t}"
+                 :: "r"(saddr), "f"(v0), "f"(v1), "r"(c4), "n"(4 * P1_RS) : "memory");
 }
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
     const int p1_col0 = 32 * warp + mg;
     const int p1_lane = 2 * c4 * P1_RS + ((mg & 1) ? P1_ODD + (p1_col0 >> 1) : (p1_col0 >> 1));
     const int xw0 = 32 * warp + mg + (c4 & 1);                    // input word, tile pair 0
-    float* const p1_scratch = p2_ring + P2_RING * 6 * P2_RS;
+    const uint32_t p1_s = (uint32_t)__cvta_generic_to_shared(p1_ring + p1_lane);
 #endif
     const int ld_w = tid < IN_WORDS ? tid : tid - IN_WORDS;      // primary word column
     const int ld_r0 = tid < IN_WORDS ? 0 : 4;                      // its rows ld_r0 .. +3
@@ -260,9 +267,9 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
                     sl[q] = (t >= IN_RING ? t - IN_RING : t) * IN_RSW;
                 }
                 // this lane's two maps of P1 row 4v+pr (lanes c4 = 3 hold the zero maps 6, 7:
-                // their stores go to a scratch area instead of a branch)
+                // predicated off inside one asm block -- no branch)
                 const int p1slot = (4 * v + pr) % P1_RING;
-                float* const p1dst = (c4 < 3) ? p1_ring + p1slot * 6 * P1_RS + p1_lane : p1_scratch;
+                const uint32_t p1dst = p1_s + 4u * (uint32_t)(p1slot * 6 * P1_RS);
                 // all four tile pairs' MMAs first, then their epilogues: the MMA latency of
                 // one pair is covered by the others
                 float dA[4][4], dB[4][4];
@@ -284,8 +291,8 @@ __global__ void __launch_bounds__(NT, S1_MIN_BLOCKS) stage1_kernel(
                 for (int g = 0; g < 4; ++g) {
                     const float m0 = fmaxf(fmaxf(dA[g][0], dA[g][2]), fmaxf(dB[g][0], dB[g][2]));
                     const float m1 = fmaxf(fmaxf(dA[g][1], dA[g][3]), fmaxf(dB[g][1], dB[g][3]));
-                    p1dst[4 * g] = act(fmaf(m0, W.l1_inv_scale, bias0));          // P1 column +8g
-                    p1dst[4 * g + P1_RS] = act(fmaf(m1, W.l1_inv_scale, bias1));
+                    st2_pred(p1dst + 16u * g, act(fmaf(m0, W.l1_inv_scale, bias0)),   // P1 column +8g
+                             act(fmaf(m1, W.l1_inv_scale, bias1)), c4);
                 }
             }
             }
