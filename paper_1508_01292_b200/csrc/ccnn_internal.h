@@ -42,6 +42,12 @@ struct __align__(16) SelNetW { // CNN2: <16,6,2>, CNN3: <2,2,25>
     float w2[B][A][9], b2[B];
     float w3[C][B][56], b3[C]; // [out][in][ky*7+kx], 7 wide x 8 tall
     float w4[C], b4;
+    // layer 1 on the tensor cores (selective.cu, A == 16): mma.m16n8k16 B fragments of
+    // w1 / 127.5 * 2^s (raw equalised pixels in, O3 folded) as fp16 hi + lo,
+    // [hi/lo][map half][lane][reg]; b1h = b1 - sum_k w1; accumulator scaled by l1_inv_scale
+    uint32_t l1frag[2][2][32][2];
+    float b1h[A];
+    float l1_inv_scale;
 };
 using Cnn2W = SelNetW<16, 6, 2>;
 using Cnn3W = SelNetW<2, 2, 25>;

@@ -23,13 +23,14 @@
 #include <type_traits>
 
 #include "ccnn_internal.h"
+#include <cuda_fp16.h>
 
 namespace ccnn {
 namespace {
 
 constexpr int kSelThreads = 288;            // 9 warps: layer-2 items (264) in one round
-constexpr int kImgRS = 56;                  // patch row: even cols [0,26), odd cols [28,53)
-constexpr int kImgOdd = 28;
+constexpr int kEW = 48;                     // words per row of the fp16 patch plane (26 used;
+                                            // 48 == 16 mod 32: rows y, y+1 on disjoint banks)
 constexpr int kP1RS = 24;                   // pooled L1 row (24 wide): even [0,12), odd [12,24)
 constexpr int kP1Odd = 12;
 
@@ -59,7 +60,8 @@ struct SelSmem {
     int hist[256];
     uint8_t lut[256];
     uint8_t patch[kPatchN + 3];
-    float img[kPatchH][kImgRS];             // E, normalised (O3), columns de-interleaved
+    uint32_t eh[kPatchH][kEW];              // E as raw fp16 pixel pairs: word j = pixels (2j, 2j+1),
+                                            // pixel 51 = 0 (exact: equalised values <= 255)
     float p2[2][6][12][12];                 // pooled layer 2 [orient][map][y][x]
     float l3[25][2][25];                    // layer-3 activations [map][orient][cell]
     float resp[2][kResp];
@@ -68,9 +70,38 @@ struct SelSmem {
 };
 constexpr size_t kP1Floats = 2 * 16 * 26 * kP1RS;   // pooled layer 1 [orient][map][y][row]
 
+// E(x, y) normalised (O3), for the FFMA layer 1 of CNN3
 __device__ __forceinline__ float img_at(const SelSmem& sm, int y, int x)
 {
-    return sm.img[y][(x & 1) ? kImgOdd + (x >> 1) : (x >> 1)];
+    const __half h = reinterpret_cast<const __half*>(&sm.eh[y][0])[x];
+    return fmaf(__half2float(h), 1.0f / 127.5f, -1.0f);
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1)
+{
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// A-fragment pair of one input row for MMA rows m (conv column x = xb + 2m) and m + 8
+// (x + 1), taps (kx0, kx0 + 1) with kx0 = 2 kb: E orientation -> pixels (x + kx0, +1) and
+// (x + 1 + kx0, +1); mirrored M(x) = E(50 - x) -> the same pairs reversed.  Two word loads.
+__device__ __forceinline__ void a_pair(const uint32_t* row, int o, int xb, int mg, int kb,
+                                       uint32_t& am, uint32_t& am8)
+{
+    if (o == 0) {
+        const int j = (xb >> 1) + mg + kb;
+        const uint32_t w0 = row[j], w1 = row[j + 1];
+        am = w0;
+        am8 = __byte_perm(w0, w1, 0x5432);
+    } else {
+        const int j = 24 - (xb >> 1) - mg - kb;
+        const uint32_t w0 = row[j], w1 = row[j + 1];
+        am = __byte_perm(w0, w1, 0x3254);
+        am8 = __byte_perm(w0, w0, 0x1032);
+    }
 }
 
 // One selective CNN (architecture R: C4x4 1->A, P, C3x3 A->B, P, C7x8 B->C, C1x1 C->1,
@@ -79,12 +110,59 @@ template <int A, int B, int C>
 __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
 {
     const int tid = threadIdx.x;
+    if constexpr (A == 16) {
+    // ---- layer 1 on the tensor cores (mma.sync m16n8k16): tile = 16 conv-1 outputs of one
+    //      conv row (MMA rows m / m+8 = columns xb+2m / xb+2m+1) x 16 taps of raw equalised
+    //      pixels (exact in fp16), N = 16 maps as two halves; weights / 127.5 * 2^s in fp16
+    //      hi + lo (two MMAs per half), bias and 2^-s after the pooling max.  A tile pair (conv
+    //      rows 2py, 2py+1) holds whole pool cells per thread; 2 orient. x 26 rows x 3 column
+    //      groups = 156 pairs over the 9 warps ----
+        const int lane = tid & 31, warp = tid >> 5;
+        const int c4 = lane & 3, mg = lane >> 2, kb = c4 & 1, ky0 = c4 >> 1;
+        uint32_t bh[2][2], bl[2][2];
+        float bias[2][2];
+#pragma unroll
+        for (int nh = 0; nh < 2; ++nh) {
+            bh[nh][0] = W.l1frag[0][nh][lane][0]; bh[nh][1] = W.l1frag[0][nh][lane][1];
+            bl[nh][0] = W.l1frag[1][nh][lane][0]; bl[nh][1] = W.l1frag[1][nh][lane][1];
+            bias[nh][0] = W.b1h[8 * nh + 2 * c4];
+            bias[nh][1] = W.b1h[8 * nh + 2 * c4 + 1];
+        }
+        for (int pi = warp; pi < 156; pi += kSelThreads / 32) {
+            const int o = pi / 78, rr = pi - o * 78, py = rr / 3, xb = 16 * (rr - 3 * py);
+            const uint32_t* r0 = &sm.eh[2 * py + ky0][0];
+            uint32_t a0, a1, a2, a3, e0, e1, e2, e3;
+            a_pair(r0, o, xb, mg, kb, a0, a1);                 // conv row 2py: rows 2py+ky
+            a_pair(r0 + 2 * kEW, o, xb, mg, kb, a2, a3);
+            a_pair(r0 + kEW, o, xb, mg, kb, e0, e1);           // conv row 2py+1
+            a_pair(r0 + 3 * kEW, o, xb, mg, kb, e2, e3);
+            const int px = (xb >> 1) + mg;                     // pooled column
+            const int col = (px & 1) ? kP1Odd + (px >> 1) : (px >> 1);
+#pragma unroll
+            for (int nh = 0; nh < 2; ++nh) {
+                float dA[4] = {0.f, 0.f, 0.f, 0.f}, dB[4] = {0.f, 0.f, 0.f, 0.f};
+                mma16816(dA, a0, a1, a2, a3, bh[nh][0], bh[nh][1]);
+                mma16816(dB, e0, e1, e2, e3, bh[nh][0], bh[nh][1]);
+                mma16816(dA, a0, a1, a2, a3, bl[nh][0], bl[nh][1]);
+                mma16816(dB, e0, e1, e2, e3, bl[nh][0], bl[nh][1]);
+                const float m0 = fmaxf(fmaxf(dA[0], dA[2]), fmaxf(dB[0], dB[2]));
+                const float m1 = fmaxf(fmaxf(dA[1], dA[3]), fmaxf(dB[1], dB[3]));
+                const int map = 8 * nh + 2 * c4;
+                p1[((o * A + map) * 26 + py) * kP1RS + col] = act(fmaf(m0, W.l1_inv_scale, bias[nh][0]));
+                p1[((o * A + map + 1) * 26 + py) * kP1RS + col] = act(fmaf(m1, W.l1_inv_scale, bias[nh][1]));
+            }
+        }
+    } else {
     // ---- layer 1: conv4x4 1->A, pool, act; item = (map group, orientation, pooled pos) ----
     constexpr int G1 = (A >= 16) ? 8 : A;           // maps per item
     constexpr int NG1 = A / G1;                     // 1248 = 39 warps of items per group
     for (int it = tid; it < NG1 * 1248; it += kSelThreads) {
         const int g = it / 1248, pos = it - g * 1248;
-        const int o = pos / 624, rem = pos - o * 624, py0 = rem / 24, px0 = rem - py0 * 24;
+        // a warp's lanes span two pooled rows (2 image rows apart, +24 banks); the mirrored
+        // orientation walks its row backwards so its image words also increase with the lane:
+        // both orientations' layer-1 reads are bank-conflict-free
+        const int o = pos / 624, rem = pos - o * 624, py0 = rem / 24;
+        const int px0 = (o == 0) ? rem - py0 * 24 : 23 - (rem - py0 * 24);
         float x[5][5];
         if (o == 0) {
 #pragma unroll
@@ -122,6 +200,7 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
             if (g == 0) body(std::integral_constant<int, 0>{});      // warp-uniform branch
             else body(std::integral_constant<int, 8>{});
         }
+    }
     }
     __syncthreads();
     // ---- layer 2: conv3x3 A->B, pool, act; item = (orientation, pooled position), all maps ----
@@ -324,11 +403,13 @@ __global__ void __launch_bounds__(kSelThreads, 2) selective_kernel(
             }
         }
         __syncthreads();
-        // ---- E normalised to [-1, 1] (O3), columns de-interleaved ----
-        for (int k = tid; k < kPatchN; k += kSelThreads) {
-            const int v = k / kPatchW, u = k - v * kPatchW;
-            sm.img[v][(u & 1) ? kImgOdd + (u >> 1) : (u >> 1)] =
-                fmaf((float)sm.lut[sm.patch[k]], 1.0f / 127.5f, -1.0f);
+        // ---- E as fp16 pixel pairs (raw equalised values; O3 is applied by the layers) ----
+        for (int k = tid; k < kPatchH * 26; k += kSelThreads) {
+            const int v = k / 26, j = k - v * 26;
+            const uint32_t p0 = sm.lut[sm.patch[v * kPatchW + 2 * j]];
+            const uint32_t p1v = (2 * j + 1 < kPatchW) ? sm.lut[sm.patch[v * kPatchW + 2 * j + 1]] : 0u;
+            const __half2 h = __floats2half2_rn((float)p0, (float)p1v);
+            sm.eh[v][j] = *reinterpret_cast<const uint32_t*>(&h);
         }
         __syncthreads();
 
