@@ -68,7 +68,7 @@ struct SelSmem {
     float wmax[kSelThreads / 32];
     int cand;
 };
-constexpr size_t kP1Floats = 2 * 16 * 26 * kP1RS;   // pooled layer 1 [orient][map][y][row]
+constexpr size_t kP1Floats = 2 * 8 * 26 * kP1RS;    // pooled layer 1, one chunk of 8 maps: [orient][map][y][row]
 
 // E(x, y) normalised (O3), for the FFMA layer 1 of CNN3
 __device__ __forceinline__ float img_at(const SelSmem& sm, int y, int x)
@@ -110,24 +110,31 @@ template <int A, int B, int C>
 __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
 {
     const int tid = threadIdx.x;
+    // layers 1-2 in chunks of AC input maps: P1 holds one chunk (both orientations), layer 2
+    // accumulates over the chunks in registers -- half the P1 smem of CNN2, so 3 CTAs fit
+    constexpr int AC = (A == 16) ? 8 : A;
+    constexpr int NCH = A / AC;
+    const bool l2_item = tid < 2 * 132;
+    const int o2 = tid / 132, pos2 = tid - o2 * 132, py2 = pos2 / 11, px2 = pos2 - py2 * 11;
+    float s2[B][4];
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s2[b][k] = W.b2[b];
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ++ch) {
     if constexpr (A == 16) {
     // ---- layer 1 on the tensor cores (mma.sync m16n8k16): tile = 16 conv-1 outputs of one
     //      conv row (MMA rows m / m+8 = columns xb+2m / xb+2m+1) x 16 taps of raw equalised
-    //      pixels (exact in fp16), N = 16 maps as two halves; weights / 127.5 * 2^s in fp16
-    //      hi + lo (two MMAs per half), bias and 2^-s after the pooling max.  A tile pair (conv
-    //      rows 2py, 2py+1) holds whole pool cells per thread; 2 orient. x 26 rows x 3 column
+    //      pixels (exact in fp16), N = the chunk's 8 maps; weights / 127.5 * 2^s in fp16
+    //      hi + lo (two MMAs), bias and 2^-s after the pooling max.  A tile pair (conv rows
+    //      2py, 2py+1) holds whole pool cells per thread; 2 orient. x 26 rows x 3 column
     //      groups = 156 pairs over the 9 warps ----
         const int lane = tid & 31, warp = tid >> 5;
         const int c4 = lane & 3, mg = lane >> 2, kb = c4 & 1, ky0 = c4 >> 1;
-        uint32_t bh[2][2], bl[2][2];
-        float bias[2][2];
-#pragma unroll
-        for (int nh = 0; nh < 2; ++nh) {
-            bh[nh][0] = W.l1frag[0][nh][lane][0]; bh[nh][1] = W.l1frag[0][nh][lane][1];
-            bl[nh][0] = W.l1frag[1][nh][lane][0]; bl[nh][1] = W.l1frag[1][nh][lane][1];
-            bias[nh][0] = W.b1h[8 * nh + 2 * c4];
-            bias[nh][1] = W.b1h[8 * nh + 2 * c4 + 1];
-        }
+        const uint32_t bh0 = W.l1frag[0][ch][lane][0], bh1 = W.l1frag[0][ch][lane][1];
+        const uint32_t bl0 = W.l1frag[1][ch][lane][0], bl1 = W.l1frag[1][ch][lane][1];
+        const float bias0 = W.b1h[8 * ch + 2 * c4], bias1 = W.b1h[8 * ch + 2 * c4 + 1];
         for (int pi = warp; pi < 156; pi += kSelThreads / 32) {
             const int o = pi / 78, rr = pi - o * 78, py = rr / 3, xb = 16 * (rr - 3 * py);
             const uint32_t* r0 = &sm.eh[2 * py + ky0][0];
@@ -138,30 +145,23 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
             a_pair(r0 + 3 * kEW, o, xb, mg, kb, e2, e3);
             const int px = (xb >> 1) + mg;                     // pooled column
             const int col = (px & 1) ? kP1Odd + (px >> 1) : (px >> 1);
-#pragma unroll
-            for (int nh = 0; nh < 2; ++nh) {
-                float dA[4] = {0.f, 0.f, 0.f, 0.f}, dB[4] = {0.f, 0.f, 0.f, 0.f};
-                mma16816(dA, a0, a1, a2, a3, bh[nh][0], bh[nh][1]);
-                mma16816(dB, e0, e1, e2, e3, bh[nh][0], bh[nh][1]);
-                mma16816(dA, a0, a1, a2, a3, bl[nh][0], bl[nh][1]);
-                mma16816(dB, e0, e1, e2, e3, bl[nh][0], bl[nh][1]);
-                const float m0 = fmaxf(fmaxf(dA[0], dA[2]), fmaxf(dB[0], dB[2]));
-                const float m1 = fmaxf(fmaxf(dA[1], dA[3]), fmaxf(dB[1], dB[3]));
-                const int map = 8 * nh + 2 * c4;
-                p1[((o * A + map) * 26 + py) * kP1RS + col] = act(fmaf(m0, W.l1_inv_scale, bias[nh][0]));
-                p1[((o * A + map + 1) * 26 + py) * kP1RS + col] = act(fmaf(m1, W.l1_inv_scale, bias[nh][1]));
-            }
+            float dA[4] = {0.f, 0.f, 0.f, 0.f}, dB[4] = {0.f, 0.f, 0.f, 0.f};
+            mma16816(dA, a0, a1, a2, a3, bh0, bh1);
+            mma16816(dB, e0, e1, e2, e3, bh0, bh1);
+            mma16816(dA, a0, a1, a2, a3, bl0, bl1);
+            mma16816(dB, e0, e1, e2, e3, bl0, bl1);
+            const float m0 = fmaxf(fmaxf(dA[0], dA[2]), fmaxf(dB[0], dB[2]));
+            const float m1 = fmaxf(fmaxf(dA[1], dA[3]), fmaxf(dB[1], dB[3]));
+            float* const dst = p1 + ((o * AC + 2 * c4) * 26 + py) * kP1RS + col;
+            dst[0] = act(fmaf(m0, W.l1_inv_scale, bias0));
+            dst[26 * kP1RS] = act(fmaf(m1, W.l1_inv_scale, bias1));
         }
     } else {
-    // ---- layer 1: conv4x4 1->A, pool, act; item = (map group, orientation, pooled pos) ----
-    constexpr int G1 = (A >= 16) ? 8 : A;           // maps per item
-    constexpr int NG1 = A / G1;                     // 1248 = 39 warps of items per group
-    for (int it = tid; it < NG1 * 1248; it += kSelThreads) {
-        const int g = it / 1248, pos = it - g * 1248;
-        // a warp's lanes span two pooled rows (2 image rows apart, +24 banks); the mirrored
-        // orientation walks its row backwards so its image words also increase with the lane:
-        // both orientations' layer-1 reads are bank-conflict-free
-        const int o = pos / 624, rem = pos - o * 624, py0 = rem / 24;
+    // ---- layer 1: conv4x4 1->A, pool, act; item = (orientation, pooled pos), all A maps ----
+    for (int it = tid; it < 1248; it += kSelThreads) {
+        // a warp's lanes span two pooled rows (2 image rows apart); the mirrored orientation
+        // walks its row backwards so its image words also increase with the lane
+        const int o = it / 624, rem = it - o * 624, py0 = rem / 24;
         const int px0 = (o == 0) ? rem - py0 * 24 : 23 - (rem - py0 * 24);
         float x[5][5];
         if (o == 0) {
@@ -175,56 +175,42 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
 #pragma unroll
                 for (int c = 0; c < 5; ++c) x[r][c] = img_at(sm, 2 * py0 + r, 50 - 2 * px0 - c);
         }
-        auto body = [&](auto M0c) {
-            constexpr int M0 = decltype(M0c)::value;
 #pragma unroll
-            for (int a = 0; a < G1; ++a) {
-                float s[4];
+        for (int a = 0; a < A; ++a) {
+            float sv[4];
 #pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    s[p] = W.b1[M0 + a];
+            for (int p = 0; p < 4; ++p) {
+                sv[p] = W.b1[a];
 #pragma unroll
-                    for (int ky = 0; ky < 4; ++ky)
+                for (int ky = 0; ky < 4; ++ky)
 #pragma unroll
-                        for (int kx = 0; kx < 4; ++kx)
-                            s[p] = fmaf(W.w1[M0 + a][ky * 4 + kx], x[(p >> 1) + ky][(p & 1) + kx], s[p]);
-                }
-                const int col = (px0 & 1) ? kP1Odd + (px0 >> 1) : (px0 >> 1);
-                p1[((o * A + M0 + a) * 26 + py0) * kP1RS + col] =
-                    act(fmaxf(fmaxf(s[0], s[1]), fmaxf(s[2], s[3])));   // pool then act
+                    for (int kx = 0; kx < 4; ++kx)
+                        sv[p] = fmaf(W.w1[a][ky * 4 + kx], x[(p >> 1) + ky][(p & 1) + kx], sv[p]);
             }
-        };
-        if constexpr (NG1 == 1) body(std::integral_constant<int, 0>{});
-        else {
-            static_assert(NG1 == 2, "map groups");
-            if (g == 0) body(std::integral_constant<int, 0>{});      // warp-uniform branch
-            else body(std::integral_constant<int, 8>{});
+            const int col = (px0 & 1) ? kP1Odd + (px0 >> 1) : (px0 >> 1);
+            p1[((o * AC + a) * 26 + py0) * kP1RS + col] =
+                act(fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3])));   // pool then act
         }
     }
     }
     __syncthreads();
-    // ---- layer 2: conv3x3 A->B, pool, act; item = (orientation, pooled position), all maps ----
-    if (tid < 2 * 132) {
-        const int o = tid / 132, pos = tid - o * 132, py0 = pos / 11, px0 = pos - py0 * 11;
-        float s[B][4];
-#pragma unroll
-        for (int b = 0; b < B; ++b)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) s[b][k] = W.b2[b];
+    // ---- layer 2 (partial over this chunk's maps): conv3x3 A->B; item = (orientation,
+    //      pooled position), all output maps ----
+    if (l2_item) {
 #pragma unroll 1
-        for (int a = 0; a < A; ++a) {               // uniform counter: LDCU [UR+imm]
-            const float* in = p1 + ((o * A + a) * 26 + 2 * py0) * kP1RS;
+        for (int a = 0; a < AC; ++a) {              // uniform counter: LDCU [UR+imm]
+            const float* in = p1 + ((o2 * AC + a) * 26 + 2 * py2) * kP1RS;
             float v[4][4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                v[r][0] = in[r * kP1RS + px0];
-                v[r][1] = in[r * kP1RS + kP1Odd + px0];
-                v[r][2] = in[r * kP1RS + px0 + 1];
-                v[r][3] = in[r * kP1RS + kP1Odd + px0 + 1];
+                v[r][0] = in[r * kP1RS + px2];
+                v[r][1] = in[r * kP1RS + kP1Odd + px2];
+                v[r][2] = in[r * kP1RS + px2 + 1];
+                v[r][3] = in[r * kP1RS + kP1Odd + px2 + 1];
             }
             constexpr int NV = SelNetW<A, B, C>::W2V;
             float wv[NV];
-            const float4* w4p = reinterpret_cast<const float4*>(W.w2v[a]);
+            const float4* w4p = reinterpret_cast<const float4*>(W.w2v[ch * AC + a]);
 #pragma unroll
             for (int k4 = 0; k4 < NV / 4; ++k4) {
                 const float4 t4 = w4p[k4];
@@ -239,12 +225,16 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
                         const float w = wv[b * 9 + ky * 3 + kx];
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
-                            s[b][k] = fmaf(w, v[(k >> 1) + ky][(k & 1) + kx], s[b][k]);
+                            s2[b][k] = fmaf(w, v[(k >> 1) + ky][(k & 1) + kx], s2[b][k]);
                     }
         }
+    }
+    if (ch + 1 < NCH) __syncthreads();             // the next chunk overwrites P1
+    }
+    if (l2_item) {
 #pragma unroll
         for (int b = 0; b < B; ++b)
-            sm.p2[o][b][py0][px0] = act(fmaxf(fmaxf(s[b][0], s[b][1]), fmaxf(s[b][2], s[b][3])));
+            sm.p2[o2][b][py2][px2] = act(fmaxf(fmaxf(s2[b][0], s2[b][1]), fmaxf(s2[b][2], s2[b][3])));
     }
     __syncthreads();
     // ---- layer 3: conv7x8 B->C, act; item = (map, orientation, cell) ----
@@ -299,7 +289,7 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kSelThreads, 2) selective_kernel(
+__global__ void __launch_bounds__(kSelThreads, 3) selective_kernel(
     const __grid_constant__ Cnn2W W2, const __grid_constant__ Cnn3W W3, const SelParams sp,
     const FrameInfo* __restrict__ frames, const LevelInfo* __restrict__ lvinfo,
     const S1Cand* __restrict__ cands, const uint32_t cand_cap, SelOut* __restrict__ out,
