@@ -39,7 +39,7 @@ def build(force=False, verbose=False, variant=None, defines=()):
 
 def _build(force, verbose, extra, objname):
     srcs = sources()
-    deps = srcs + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "ccnn.h"),
+    deps = srcs + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "ccnn.h"),
                                                           __file__]
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(map(os.path.getmtime, deps)):
         return LIB

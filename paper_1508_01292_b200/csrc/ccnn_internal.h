@@ -33,6 +33,9 @@ struct __align__(16) Cnn1W {   // 797 weights + re-arranged copies for the stage
     uint32_t l1frag[2][32][2];
     float b1h[8];
     float l1_inv_scale;
+    // layer 2 on the tensor cores (stage1_tc.cu): w2 * 2^s2 (max |w'| in [8, 16)) as fp16
+    // hi + lo; the accumulator is scaled back by l2_inv_scale = 2^-s2
+    float l2_inv_scale;
 };
 template <int A, int B, int C>
 struct __align__(16) SelNetW { // CNN2: <16,6,2>, CNN3: <2,2,25>
@@ -153,6 +156,16 @@ void launch_stage1(const Cnn1W& w, float T1, const uint8_t* levels, const LevelI
 int stage1_band_width();          // TW of the compiled stage-1 kernel
 int stage1_grid(int sm_count);    // CTAs of the persistent stage-1 launch
 int stage1_task_cost(int nrows);  // relative cost of a task (super-steps)
+// stage 1 with layers 1-2 on tcgen05 (stage1_tc.cu, the default): same task list format,
+// band width stage1_tc_band_width(); d_bmats = the B matrices built by stage1_tc_bmats
+void launch_stage1_tc(const Cnn1W& w, float T1, const uint16_t* d_bmats, const uint8_t* levels,
+                      const LevelInfo* d_levels, const S1Task* d_tasks, const int32_t* d_cta_first, int grid,
+                      S1Cand* cands, uint32_t cand_cap, Ctrl* ctrl, float* dbg_map, cudaStream_t s);
+int stage1_tc_band_width();
+int stage1_tc_grid(int sm_count);
+int stage1_tc_task_cost(int nrows);
+int stage1_tc_bmats(const Cnn1W& w, uint16_t* out);   // fills out (kStage1TcBmatHalves), returns count
+constexpr int kStage1TcBmatHalves = (8 + 16) * 48 * 16;
 // selective unit (stage 2/3), persistent over the survivor queue
 struct SelParams { float T2a, T2b; int32_t Tnn, rule; };
 void launch_selective(const Cnn2W& w2, const Cnn3W& w3, SelParams sp, const FrameInfo* d_frames,

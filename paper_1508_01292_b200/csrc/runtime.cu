@@ -6,6 +6,7 @@
 // -ffp-contract=off so no multiply-add is fused and every value is bit-identical to
 // the oracle's independent implementation.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -83,6 +84,8 @@ struct ccnn_ctx {
     std::vector<S1Task> tasks;          // grouped by CTA (LPT schedule)
     std::vector<int32_t> cta_first;     // stage1_grid + 1 offsets into tasks
     int s1_grid = 0;
+    bool s1_tc = true;                  // stage 1 on tcgen05 (stage1_tc.cu); CCNN_S1_LEGACY=1 -> stage1.cu
+    DevBuf s1_bmats;                    // its B matrices
     std::vector<uint32_t> tabs;
     int64_t arena_bytes = 0;            // all levels of all frames
     int64_t map_total = 0;              // dense stage-1 map floats (debug)
@@ -216,6 +219,12 @@ void unpack_cnn1(const float* w, Cnn1W& o)
             }
             o.b1h[m] = (float)b;
         }
+    }
+    {                                                // tensor-core layer-2 scale (stage1_tc.cu)
+        double mx = 0.0;
+        for (int k = 0; k < 324; ++k) mx = std::max(mx, std::fabs((double)(&o.w2[0][0][0])[k]));
+        const int e = mx > 0.0 ? (int)std::floor(std::log2(mx)) : 0;
+        o.l2_inv_scale = (float)std::ldexp(1.0, e - 3);
     }
     for (int ci = 0; ci < 6; ++ci) {                 // vector-friendly copies (stage1.cu)
         for (int k = 0; k < 56; ++k) o.w2v[ci][k] = k < 54 ? o.w2[k / 9][ci][k % 9] : 0.f;
@@ -418,7 +427,8 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
     // slack so that the stage-1 loader's last (clamped) word read stays in bounds
     c->arena_bytes = round_up(off + 256, 256);
     c->map_total = map_off;
-    const int TW = stage1_band_width();
+    const int TW = c->s1_tc ? stage1_tc_band_width() : stage1_band_width();
+    auto task_cost = [&](int nrows) { return c->s1_tc ? stage1_tc_task_cost(nrows) : stage1_task_cost(nrows); };
     // segment height: the tallest segments (least vertical halo recompute) whose largest
     // task still fits in half the average load of a CTA slot, so the dynamic list schedule
     // balances (ccnn_params.segment_rows > 0 forces a height)
@@ -489,8 +499,8 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
             make_tasks(seg, one);
             int64_t total = 0, biggest = 0;
             for (const S1Task& t : one) {
-                total += stage1_task_cost(t.nrows);
-                biggest = std::max<int64_t>(biggest, stage1_task_cost(t.nrows));
+                total += task_cost(t.nrows);
+                biggest = std::max<int64_t>(biggest, task_cost(t.nrows));
             }
             if (2 * biggest * c->s1_grid <= total) break;
         }
@@ -559,7 +569,19 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
     ctx->max_batch = p->max_batch;
     ctx->queue_cap = p->queue_capacity > 0 ? p->queue_capacity : 4096;
     ctx->seg_rows_param = p->segment_rows;
-    ctx->s1_grid = stage1_grid(ctx->sm_count);
+    {
+        const char* leg = std::getenv("CCNN_S1_LEGACY");
+        ctx->s1_tc = !(leg && leg[0] == '1');
+    }
+    ctx->s1_grid = ctx->s1_tc ? stage1_tc_grid(ctx->sm_count) : stage1_grid(ctx->sm_count);
+    if (const char* v = std::getenv("CCNN_VERBOSE"))
+        if (v[0] == '1') std::fprintf(stderr, "ccnn: stage 1 %s, grid %d\n", ctx->s1_tc ? "tcgen05" : "legacy", ctx->s1_grid);
+    if (ctx->s1_tc) {
+        std::vector<uint16_t> bm(kStage1TcBmatHalves);
+        stage1_tc_bmats(ctx->w1, bm.data());
+        CU(ctx->s1_bmats.ensure(bm.size() * 2));
+        CU(cudaMemcpy(ctx->s1_bmats.p, bm.data(), bm.size() * 2, cudaMemcpyHostToDevice));
+    }
     CU(cudaGetLastError());
     for (auto& sl : ctx->slot) {
         CU(cudaMallocHost(&sl.h_ctrl, sizeof(Ctrl)));
@@ -601,7 +623,7 @@ void ccnn_destroy(ccnn_ctx* ctx)
     drop_textures(ctx, nullptr, 0);
     for (DevBuf* b : {&ctx->arena, &ctx->d_levels, &ctx->d_tasks, &ctx->d_cta_first, &ctx->d_tabs, &ctx->d_ptiles,
                       &ctx->cands, &ctx->selout, &ctx->dbg_resp, &ctx->acc, &ctx->staging, &ctx->counts,
-                      &ctx->dbg_map})
+                      &ctx->dbg_map, &ctx->s1_bmats})
         b->release();
     for (auto& sl : ctx->slot) {
         sl.frames.release();
@@ -826,10 +848,16 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
                    ctx->d_levels.as<LevelInfo>(), ctx->d_ptiles.as<uint32_t>(),
                    ctx->d_tabs.as<uint32_t>(), s);
     CU(cudaEventRecord(sl.ev[3], s));
-    launch_stage1(ctx->w1, ctx->T1, ctx->arena.as<uint8_t>(), ctx->d_levels.as<LevelInfo>(),
-                  ctx->d_tasks.as<S1Task>(), ctx->d_cta_first.as<int32_t>(),
-                  (int)ctx->cta_first.size() - 1, ctx->cands.as<S1Cand>(), cand_cap, dctrl,
-                  dbg1 ? ctx->dbg_map.as<float>() : nullptr, s);
+    if (ctx->s1_tc)
+        launch_stage1_tc(ctx->w1, ctx->T1, ctx->s1_bmats.as<uint16_t>(), ctx->arena.as<uint8_t>(),
+                         ctx->d_levels.as<LevelInfo>(), ctx->d_tasks.as<S1Task>(), ctx->d_cta_first.as<int32_t>(),
+                         (int)ctx->cta_first.size() - 1, ctx->cands.as<S1Cand>(), cand_cap, dctrl,
+                         dbg1 ? ctx->dbg_map.as<float>() : nullptr, s);
+    else
+        launch_stage1(ctx->w1, ctx->T1, ctx->arena.as<uint8_t>(), ctx->d_levels.as<LevelInfo>(),
+                      ctx->d_tasks.as<S1Task>(), ctx->d_cta_first.as<int32_t>(),
+                      (int)ctx->cta_first.size() - 1, ctx->cands.as<S1Cand>(), cand_cap, dctrl,
+                      dbg1 ? ctx->dbg_map.as<float>() : nullptr, s);
     CU(cudaEventRecord(sl.ev[4], s));
     launch_selective(ctx->w2, ctx->w3, ctx->sp, dfi, ctx->d_levels.as<LevelInfo>(),
                      ctx->cands.as<S1Cand>(), cand_cap, ctx->selout.as<SelOut>(),
