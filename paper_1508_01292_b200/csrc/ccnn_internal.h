@@ -36,6 +36,7 @@ struct __align__(16) Cnn1W {   // 797 weights + re-arranged copies for the stage
     // layer 2 on the tensor cores (stage1_tc.cu): w2 * 2^s2 (max |w'| in [8, 16)) as fp16
     // hi + lo; the accumulator is scaled back by l2_inv_scale = 2^-s2
     float l2_inv_scale;
+    float l3_inv_scale;        // likewise for layer 3 (w3)
 };
 template <int A, int B, int C>
 struct __align__(16) SelNetW { // CNN2: <16,6,2>, CNN3: <2,2,25>
@@ -165,7 +166,7 @@ int stage1_tc_band_width();
 int stage1_tc_grid(int sm_count);
 int stage1_tc_task_cost(int nrows);
 int stage1_tc_bmats(const Cnn1W& w, uint16_t* out);   // fills out (kStage1TcBmatHalves), returns count
-constexpr int kStage1TcBmatHalves = (8 + 16) * 48 * 16;
+constexpr int kStage1TcBmatHalves = (8 + 16) * 48 * 16 + 6 * 24 * 16;
 // selective unit (stage 2/3), persistent over the survivor queue
 struct SelParams { float T2a, T2b; int32_t Tnn, rule; };
 void launch_selective(const Cnn2W& w2, const Cnn3W& w3, SelParams sp, const FrameInfo* d_frames,

@@ -225,6 +225,10 @@ void unpack_cnn1(const float* w, Cnn1W& o)
         for (int k = 0; k < 324; ++k) mx = std::max(mx, std::fabs((double)(&o.w2[0][0][0])[k]));
         const int e = mx > 0.0 ? (int)std::floor(std::log2(mx)) : 0;
         o.l2_inv_scale = (float)std::ldexp(1.0, e - 3);
+        double m3 = 0.0;
+        for (int k = 0; k < 360; ++k) m3 = std::max(m3, std::fabs((double)(&o.w3[0][0][0])[k]));
+        const int e3 = m3 > 0.0 ? (int)std::floor(std::log2(m3)) : 0;
+        o.l3_inv_scale = (float)std::ldexp(1.0, e3 - 3);
     }
     for (int ci = 0; ci < 6; ++ci) {                 // vector-friendly copies (stage1.cu)
         for (int k = 0; k < 56; ++k) o.w2v[ci][k] = k < 54 ? o.w2[k / 9][ci][k % 9] : 0.f;

@@ -62,16 +62,23 @@ constexpr int PL_PAR = PL_E * 16;              // 2112 B == 64 mod 128: conflict
 constexpr int PL_HL = 2 * PL_PAR;
 constexpr int PL_SLOT = 2 * PL_HL;
 constexpr int P1_RING = 6;
-constexpr int P2_W = 132;                      // P2 row width (128 + the window reach)
-constexpr int OFF_B1 = 0, OFF_B2 = OFF_B1 + B1_BYTES, OFF_PL = OFF_B2 + B2_BYTES;
+constexpr int B3_BYTES = 6 * 24 * 16 * 2;      // layer-3 B: [kx pair 3][A part 2] x (24 x 16 fp16)
+constexpr int BMAT3 = 24 * 16 * 2;             // [k chunk 2][n 24][8]
+constexpr int P2_E = 136;                      // P2 entries per (buffer, part): 128 written + reach
+constexpr int P2_HL = P2_E * 16;
+constexpr int P2_BUF = 2 * P2_HL;
+constexpr int OFF_B1 = 0, OFF_B2 = OFF_B1 + B1_BYTES, OFF_B3 = OFF_B2 + B2_BYTES;
+constexpr int OFF_PL = OFF_B3 + B3_BYTES;
 constexpr int OFF_P2 = OFF_PL + P1_RING * PL_SLOT;
-constexpr int SMEM_BYTES = OFF_P2 + 2 * 6 * P2_W * 4;
+constexpr int SMEM_BYTES = OFF_P2 + 2 * P2_BUF;
 // TMEM columns
 constexpr uint32_t TM_A = 0;                   // A ring: tile t at 32 t, image row slot s at +4 s
 constexpr uint32_t TM_D1 = 64;                 // layer-1 accumulators: tile t at 64 + 48 t
 constexpr uint32_t TM_D2 = 160;                // layer-2 accumulator (48)
+constexpr uint32_t TM_D3 = 208;                // layer-3 accumulator (24)
 constexpr uint32_t TM_COLS = 256;
 constexpr uint32_t IDESC = tc05::idesc_f16(128, 48);
+constexpr uint32_t IDESC3 = tc05::idesc_f16(128, 24);
 
 __device__ __forceinline__ uint32_t h2_of(uint32_t word, uint32_t sel)
 {
@@ -84,6 +91,29 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b)
 {
     const __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ void ld24(uint32_t taddr, float (&v)[24])
+{
+    uint32_t r[24];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%24];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%25];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23])
+        : "r"(taddr), "r"(taddr + 16u)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 24; ++i) v[i] = __uint_as_float(r[i]);
+}
+// fp32 pair -> fp16 hi pair + fp16 lo pair (v - hi), packed
+__device__ __forceinline__ void split_h2(float a, float b, uint32_t& hi, uint32_t& lo)
+{
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = pack_h2(a - hf.x, b - hf.y);
 }
 __device__ __forceinline__ void ld48(uint32_t taddr, float (&v)[48])
 {
@@ -116,7 +146,7 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ int s_task;
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) uint64_t bar_l1, bar_l2;
+    __shared__ __align__(8) uint64_t bar_l1, bar_l2, bar_l3;
 
     const int tid = threadIdx.x;
     // warp index through shfl: provably warp-uniform, so role branches stay on the uniform
@@ -129,14 +159,15 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     {
         const uint4* src = reinterpret_cast<const uint4*>(bmats);
         uint4* dst = reinterpret_cast<uint4*>(smem + OFF_B1);
-        for (int i = tid; i < (B1_BYTES + B2_BYTES) / 16; i += NT) dst[i] = src[i];
+        for (int i = tid; i < (B1_BYTES + B2_BYTES + B3_BYTES) / 16; i += NT) dst[i] = src[i];
         uint4* z = reinterpret_cast<uint4*>(smem + OFF_PL);
-        for (int i = tid; i < (P1_RING * PL_SLOT + 2 * 6 * P2_W * 4) / 16; i += NT) z[i] = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < (SMEM_BYTES - OFF_PL) / 16; i += NT) z[i] = make_uint4(0, 0, 0, 0);
     }
     if (mma_warp) tc05::tmem_alloc(&s_tmem, TM_COLS);
     if (tid == 0) {
         tc05::mbar_init(&bar_l1, 1);
         tc05::mbar_init(&bar_l2, 1);
+        tc05::mbar_init(&bar_l3, 1);
         tc05::mbar_fence_init();
     }
     tc05::fence_async_smem();
@@ -144,12 +175,11 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     __syncthreads();
     tc05::fence_after();
     const uint32_t tm = s_tmem;
-    uint32_t ph_l1 = 0, ph_l2 = 0;           // completed phases of each mbarrier
+    uint32_t ph_l1 = 0, ph_l2 = 0, ph_l3 = 0;   // completed phases of each mbarrier
 
     const uint32_t s_base = tc05::smem_u32(smem);
     const int m = 32 * (warp & 3) + lane;    // TMEM lane / P2 column / window column
     const uint32_t t_lane = (uint32_t)(32 * (warp & 3)) << 16;
-    float* const p2buf = reinterpret_cast<float*>(smem + OFF_P2);
 
     const int n_tasks = cta_first[gridDim.x];
     for (;;) {
@@ -225,12 +255,7 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                         }
                         uint32_t hi[3], lo[3];
 #pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            const __half2 h = __floats2half2_rn(v[2 * c], v[2 * c + 1]);
-                            const float2 hf = __half22float2(h);
-                            hi[c] = *reinterpret_cast<const uint32_t*>(&h);
-                            lo[c] = pack_h2(v[2 * c] - hf.x, v[2 * c + 1] - hf.y);
-                        }
+                        for (int c = 0; c < 3; ++c) split_h2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
                         const int slot = (2 * k + rr) % P1_RING;
                         uint8_t* e = smem + OFF_PL + slot * PL_SLOT + (x1 & 1) * PL_PAR + (x1 >> 1) * 16;
                         *reinterpret_cast<uint4*>(e) = make_uint4(hi[0], hi[1], hi[2], 0u);
@@ -238,19 +263,25 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                     }
                 }
             };
-            // layer-2 epilogue: P2 row -> p2buf[b] (column m)
+            // layer-2 epilogue: P2 row -> P2 buffer b as fp16 hi / lo entries (column m)
             auto l2_epilogue = [&](int b) {
                 float d[48];
                 ld48(tm + t_lane + TM_D2, d);
-                float* dst = p2buf + b * 6 * P2_W + m;
+                float v[6];
 #pragma unroll
                 for (int o = 0; o < 6; ++o) {
-                    float s[4];
+                    float s4[4];
 #pragma unroll
-                    for (int p = 0; p < 4; ++p) s[p] = d[p * 6 + o] + d[24 + p * 6 + o];
-                    const float mx = fmaxf(fmaxf(s[0], s[1]), fmaxf(s[2], s[3]));
-                    dst[o * P2_W] = act(fmaf(mx, W.l2_inv_scale, W.b2[o]));
+                    for (int p = 0; p < 4; ++p) s4[p] = d[p * 6 + o] + d[24 + p * 6 + o];
+                    const float mx = fmaxf(fmaxf(s4[0], s4[1]), fmaxf(s4[2], s4[3]));
+                    v[o] = act(fmaf(mx, W.l2_inv_scale, W.b2[o]));
                 }
+                uint32_t hi[3], lo[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) split_h2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
+                uint8_t* e = smem + OFF_P2 + b * P2_BUF + m * 16;
+                *reinterpret_cast<uint4*>(e) = make_uint4(hi[0], hi[1], hi[2], 0u);
+                *reinterpret_cast<uint4*>(e + P2_HL) = make_uint4(lo[0], lo[1], lo[2], 0u);
             };
 
             // the window column this thread emits
@@ -261,37 +292,27 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
             const bool e_col = (j3 < TW) && (j3 >= PE.J) && (j3 < PE.J + PE.w);
             const LevelInfo& LE = lvinfo[e_level];
             const int e_rows = min(nrows, LE.ny - T.y0);
+            // acc3[mm][i]: layer-3 map mm of window row (P2 row p) - 5 + i, in B-matrix scale
             float acc3[2][6];
 #pragma unroll
             for (int mm = 0; mm < 2; ++mm)
 #pragma unroll
                 for (int i = 0; i < 6; ++i) acc3[mm][i] = 0.f;
-            // layer 3 over P2 row q (buffer b), then the finished window row q - 5
-            auto l3_row = [&](int q, int b) {
-                const float* p2 = p2buf + b * 6 * P2_W;
-#pragma unroll                                     // weights: LDCU.128 -> FFMA R, R, UR
-                for (int ci = 0; ci < 6; ++ci) {
-                    float xv[5];
+            // layer-3 epilogue of P2 row p: its contributions to the 6 window rows it reaches
+            // (TMEM column (w part) * 12 + ky * 2 + mm), then the finished window row p - 5
+            auto l3_epilogue = [&](int p) {
+                float d[24];
+                ld24(tm + t_lane + TM_D3, d);
 #pragma unroll
-                    for (int kx = 0; kx < 5; ++kx) xv[kx] = p2[ci * P2_W + j3 + kx];
-                    float wv[60];
-                    const float4* w4p = reinterpret_cast<const float4*>(W.w3v[ci]);
+                for (int i = 0; i < 6; ++i)
 #pragma unroll
-                    for (int k4 = 0; k4 < 15; ++k4) {
-                        const float4 t4 = w4p[k4];
-                        wv[4 * k4] = t4.x; wv[4 * k4 + 1] = t4.y; wv[4 * k4 + 2] = t4.z; wv[4 * k4 + 3] = t4.w;
+                    for (int mm = 0; mm < 2; ++mm) {
+                        const int n = (5 - i) * 2 + mm;
+                        acc3[mm][i] += d[n] + d[12 + n];
                     }
-#pragma unroll
-                    for (int i = 0; i < 6; ++i)
-#pragma unroll
-                        for (int mm = 0; mm < 2; ++mm)
-#pragma unroll
-                            for (int kx = 0; kx < 5; ++kx)
-                                acc3[mm][i] = fmaf(wv[(i * 2 + mm) * 5 + kx], xv[kx], acc3[mm][i]);
-                }
-                const int o = q - 5;                        // finished window row (task-relative)
-                const float a0 = act(acc3[0][0] + W.b3[0]);
-                const float a1 = act(acc3[1][0] + W.b3[1]);
+                const int o = p - 5;                        // finished window row (task-relative)
+                const float a0 = act(fmaf(acc3[0][0], W.l3_inv_scale, W.b3[0]));
+                const float a1 = act(fmaf(acc3[1][0], W.l3_inv_scale, W.b3[1]));
 #pragma unroll
                 for (int mm = 0; mm < 2; ++mm) {
 #pragma unroll
@@ -349,43 +370,46 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 tc05::st_wait();
                 sync_for_mma();                                // -> L1(1)
             }
+            // step q: consume L1(q+1), L2(q-1), L3(q-2); the MMA warp then issues L1(q+2),
+            // L2(q), L3(q-1)
 #pragma unroll 1
-            for (int q = 0; q < NQ; ++q) {
+            for (int q = 0; q <= NQ + 1; ++q) {
                 const bool more = q + 2 <= NQ;                 // unit q+2 exists
                 uint32_t wx[4][2];
                 if (more) {
 #pragma unroll
                     for (int r = 0; r < 4; ++r) fetch(4 * q + 12 + r, wx[r]);
                 }
-                tc05::mbar_wait(&bar_l1, ph_l1 & 1); ++ph_l1;  // L1(q+1) done
-                tc05::fence_after();
-                l1_epilogue(q + 1);
-                if (q >= 1) {
-                    tc05::mbar_wait(&bar_l2, ph_l2 & 1); ++ph_l2;   // L2(q-1) done
+                if (q + 1 <= NQ) {
+                    tc05::mbar_wait(&bar_l1, ph_l1 & 1); ++ph_l1;      // L1(q+1) done
+                    tc05::fence_after();
+                    l1_epilogue(q + 1);
+                }
+                if (q >= 1 && q <= NQ) {
+                    tc05::mbar_wait(&bar_l2, ph_l2 & 1); ++ph_l2;      // L2(q-1) done
                     tc05::fence_after();
                     l2_epilogue((q - 1) & 1);
+                }
+                if (q >= 2) {
+                    tc05::mbar_wait(&bar_l3, ph_l3 & 1); ++ph_l3;      // L3(q-2) done
+                    tc05::fence_after();
+                    l3_epilogue(q - 2);
                 }
                 if (more) {
 #pragma unroll
                     for (int r = 0; r < 4; ++r) put(4 * q + 12 + r, wx[r]);
                 }
                 tc05::st_wait();
-                sync_for_mma();                                // -> L1(q+2), L2(q)
-                if (q >= 1) l3_row(q - 1, (q - 1) & 1);
+                sync_for_mma();                                // -> L1(q+2), L2(q), L3(q-1)
             }
-            tc05::mbar_wait(&bar_l2, ph_l2 & 1); ++ph_l2;      // L2(NQ-1)
-            tc05::fence_after();
-            l2_epilogue((NQ - 1) & 1);
-            tc05::fence_before();
-            __syncthreads();                                   // p2buf visible (named: all)
-            l3_row(NQ - 1, (NQ - 1) & 1);
         } else {
             // ============================ MMA warp ============================
             const uint64_t bd1 = tc05::sdesc(s_base + OFF_B1, 48 * 16, 128);
             const uint64_t bd2 = tc05::sdesc(s_base + OFF_B2, 48 * 16, 128);
             const uint64_t ad2 = tc05::sdesc(s_base + OFF_PL, PL_PAR, 128);
+            const uint64_t bd3 = tc05::sdesc(s_base + OFF_B3, 24 * 16, 128);
+            const uint64_t ad3 = tc05::sdesc(s_base + OFF_P2, 16, 128);
             auto issue_l1 = [&](int k) {
-                tc05::fence_after();
                 if (tc05::elect_one()) {
 #pragma unroll
                     for (int t = 0; t < 2; ++t)
@@ -402,7 +426,6 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 __syncwarp();
             };
             auto issue_l2 = [&](int q) {
-                tc05::fence_after();
                 if (tc05::elect_one()) {
 #pragma unroll
                     for (int dy = 0; dy < 4; ++dy) {
@@ -420,17 +443,36 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 }
                 __syncwarp();
             };
+            // layer 3 of P2 row p: row m = window column j, K = 16 = P2 entries j+kx, j+kx+1
+            // (LBO = one entry), N = 24 = {w hi, w lo} x 6 kernel rows x 2 maps
+            auto issue_l3 = [&](int p) {
+                if (tc05::elect_one()) {
+#pragma unroll
+                    for (int kp = 0; kp < 3; ++kp)
+#pragma unroll
+                        for (int ha = 0; ha < 2; ++ha) {
+                            const uint64_t a = ad3 + (uint64_t)(((p & 1) * P2_BUF + ha * P2_HL + kp * 32) >> 4);
+                            const uint64_t b = bd3 + (uint64_t)((kp * 2 + ha) * (BMAT3 >> 4));
+                            tc05::mma_f16(tm + TM_D3, a, b, IDESC3, (kp | ha) != 0);
+                        }
+                    tc05::commit(&bar_l3);
+                }
+                __syncwarp();
+            };
             __syncthreads();                                   // rows 0..7 in TMEM
+            tc05::fence_after();
             issue_l1(0);
             __syncthreads();                                   // rows 8..11, P1 rows 0, 1
+            tc05::fence_after();
             issue_l1(1);
 #pragma unroll 1
-            for (int q = 0; q < NQ; ++q) {
-                __syncthreads();                               // P1 rows 2q+2, 2q+3; rows of unit q+2
+            for (int q = 0; q <= NQ + 1; ++q) {
+                __syncthreads();
+                tc05::fence_after();
                 if (q + 2 <= NQ) issue_l1(q + 2);
-                issue_l2(q);
+                if (q < NQ) issue_l2(q);
+                if (q >= 1 && q <= NQ) issue_l3(q - 1);
             }
-            __syncthreads();                                   // final p2buf barrier
         }
     }
     tc05::fence_before();
@@ -474,7 +516,7 @@ int stage1_tc_bmats(const Cnn1W& w, uint16_t* out)
         out[mat * (BMAT / 2) + (kk >> 3) * 48 * 8 + n * 8 + (kk & 7)] = __half_as_ushort(__float2half_rn(v));
     };
     const int total = (B1_BYTES + B2_BYTES) / 2;
-    std::fill(out, out + total, (uint16_t)0);
+    std::fill(out, out + total + B3_BYTES / 2, (uint16_t)0);
     // layer 1: mat = pair p * 2 + part; n = rr * 24 + pos * 6 + o; kk = e * 8 + c
     const double sc1 = 1.0 / (double)w.l1_inv_scale;
     for (int p = 0; p < 4; ++p)
@@ -510,7 +552,27 @@ int stage1_tc_bmats(const Cnn1W& w, uint16_t* out)
                                 put(8 + (dy * 2 + d) * 2 + ha, wh * 24 + pos * 6 + o, kk, wh ? wp - hi : wp);
                             }
                 }
-    return total;
+    // layer 3: mat = 24 * 2 (B1 + B2 in BMAT units) then [kx pair kp 3][A part 2] (BMAT3 each);
+    // n = w part * 12 + ky * 2 + mm; kk = c * 8 + ch, kx = 2 kp + c
+    uint16_t* out3 = out + (B1_BYTES + B2_BYTES) / 2;
+    const double sc3 = 1.0 / (double)w.l3_inv_scale;
+    for (int kp = 0; kp < 3; ++kp)
+        for (int ha = 0; ha < 2; ++ha)
+            for (int wh = 0; wh < 2; ++wh) {
+                if (ha && wh) continue;
+                for (int ky = 0; ky < 6; ++ky)
+                    for (int mm = 0; mm < 2; ++mm)
+                        for (int kk = 0; kk < 16; ++kk) {
+                            const int kx = 2 * kp + (kk >> 3), ch = kk & 7;
+                            if (kx > 4 || ch >= 6) continue;
+                            const float wp = (float)((double)w.w3[mm][ch][ky * 5 + kx] * sc3);
+                            const float hi = __half2float(__float2half_rn(wp));
+                            const int n = wh * 12 + ky * 2 + mm;
+                            out3[(kp * 2 + ha) * (BMAT3 / 2) + (kk >> 3) * 24 * 8 + n * 8 + (kk & 7)] =
+                                __half_as_ushort(__float2half_rn(wh ? wp - hi : wp));
+                        }
+            }
+    return total + B3_BYTES / 2;
 }
 
 void launch_stage1_tc(const Cnn1W& w, float T1, const uint16_t* d_bmats, const uint8_t* levels,
