@@ -79,6 +79,10 @@ constexpr uint32_t TM_D3 = 208;                // layer-3 accumulator (24)
 constexpr uint32_t TM_COLS = 256;
 constexpr uint32_t IDESC = tc05::idesc_f16(128, 48);
 constexpr uint32_t IDESC3 = tc05::idesc_f16(128, 24);
+// lo(A) parts multiply only the w-hi columns: N = 24 (layer 2), 16 (layer 3: 12 used), same B
+// matrices (their k-chunk stride stays the full width)
+constexpr uint32_t IDESC_LO = tc05::idesc_f16(128, 24);
+constexpr uint32_t IDESC3_LO = tc05::idesc_f16(128, 16);
 
 __device__ __forceinline__ uint32_t h2_of(uint32_t word, uint32_t sel)
 {
@@ -370,8 +374,8 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 tc05::st_wait();
                 sync_for_mma();                                // -> L1(1)
             }
-            // step q: consume L1(q+1), L2(q-1), L3(q-2); the MMA warp then issues L1(q+2),
-            // L2(q), L3(q-1)
+            // step q: consume L3(q-2), L1(q+1), L2(q-1) (issue order: the heavy L2 last); the MMA
+            // warp then issues L3(q-1), L1(q+2), L2(q)
 #pragma unroll 1
             for (int q = 0; q <= NQ + 1; ++q) {
                 const bool more = q + 2 <= NQ;                 // unit q+2 exists
@@ -379,6 +383,11 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 if (more) {
 #pragma unroll
                     for (int r = 0; r < 4; ++r) fetch(4 * q + 12 + r, wx[r]);
+                }
+                if (q >= 2) {
+                    tc05::mbar_wait(&bar_l3, ph_l3 & 1); ++ph_l3;      // L3(q-2) done
+                    tc05::fence_after();
+                    l3_epilogue(q - 2);
                 }
                 if (q + 1 <= NQ) {
                     tc05::mbar_wait(&bar_l1, ph_l1 & 1); ++ph_l1;      // L1(q+1) done
@@ -389,11 +398,6 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                     tc05::mbar_wait(&bar_l2, ph_l2 & 1); ++ph_l2;      // L2(q-1) done
                     tc05::fence_after();
                     l2_epilogue((q - 1) & 1);
-                }
-                if (q >= 2) {
-                    tc05::mbar_wait(&bar_l3, ph_l3 & 1); ++ph_l3;      // L3(q-2) done
-                    tc05::fence_after();
-                    l3_epilogue(q - 2);
                 }
                 if (more) {
 #pragma unroll
@@ -436,7 +440,7 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                             for (int ha = 0; ha < 2; ++ha) {
                                 const uint64_t a = ad2 + (uint64_t)((slot_off + ha * PL_HL + d * 16) >> 4);
                                 const uint64_t b = bd2 + (uint64_t)(((dy * 2 + d) * 2 + ha) * (BMAT >> 4));
-                                tc05::mma_f16(tm + TM_D2, a, b, IDESC, (dy | d | ha) != 0);
+                                tc05::mma_f16(tm + TM_D2, a, b, ha ? IDESC_LO : IDESC, (dy | d | ha) != 0);
                             }
                     }
                     tc05::commit(&bar_l2);
@@ -453,7 +457,7 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                         for (int ha = 0; ha < 2; ++ha) {
                             const uint64_t a = ad3 + (uint64_t)(((p & 1) * P2_BUF + ha * P2_HL + kp * 32) >> 4);
                             const uint64_t b = bd3 + (uint64_t)((kp * 2 + ha) * (BMAT3 >> 4));
-                            tc05::mma_f16(tm + TM_D3, a, b, IDESC3, (kp | ha) != 0);
+                            tc05::mma_f16(tm + TM_D3, a, b, ha ? IDESC3_LO : IDESC3, (kp | ha) != 0);
                         }
                     tc05::commit(&bar_l3);
                 }
@@ -469,9 +473,9 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
             for (int q = 0; q <= NQ + 1; ++q) {
                 __syncthreads();
                 tc05::fence_after();
+                if (q >= 1 && q <= NQ) issue_l3(q - 1);
                 if (q + 2 <= NQ) issue_l1(q + 2);
                 if (q < NQ) issue_l2(q);
-                if (q >= 1 && q <= NQ) issue_l3(q - 1);
             }
         }
     }
