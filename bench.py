@@ -282,6 +282,11 @@ def main():
         peaks = measured_peaks()
         sm_max = float(peaks.get("sm_max_mhz", 1965.0))
         fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12     # FFMA pipe peak
+        # stage 1 runs its three conv layers as fp16 tcgen05 MMAs (exact pixels, hi+lo split
+        # weights / activations, fp32 accumulators): the dense fp16 tensor peak binds.  The
+        # kernel is timed inside a long step -> the sustained measured figure (bf16 and fp16
+        # share the nominal rate, B200_PROFILING.md)
+        tc_peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 2250.0)))
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "stage1_traffic.json")
         if os.path.exists(tpath):
@@ -294,7 +299,7 @@ def main():
             "metric": "4K UHD frames/s (min face 60px)",
             "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": value / PAPER_4K_FPS, "dtype": "f32",
+            "scaling": "weak", "vs_baseline": value / PAPER_4K_FPS, "dtype": "f16*f16->f32 (hi+lo split MMAs, f32 epilogues)",
             "data": "synthetic",
             "config": {"workload": cfg.name, "frames_per_step_per_gpu": batch, "W": cfg.width,
                        "H": cfg.height, "min_face": cfg.min_face, "scale_step": cfg.scale_step,
@@ -306,12 +311,16 @@ def main():
             "stage_ms_per_step": {k: v for k, v in zip(["h2d", "pyramid", "stage1", "selective", "nms_out"],
                                                         stats["ms"])},
             "table1_counts_last_step": {k: stats[k] for k in ("windows", "stage1", "stage2", "stage3", "nms")},
-            "roofline": {"bound": "alu", "achieved": achieved_tflops, "peak": fp32_peak,
-                         "unit": "TFLOP/s", "frac": achieved_tflops / fp32_peak, "traffic": traffic,
-                         "kernel": "stage1_kernel",
-                         "peak_note": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json); "
-                                      "achieved = algorithmic fp32 FLOPs (layers 2-4 on FFMA, layer 1 as "
-                                      "fp16 hi+lo mma.sync, DESIGN.md K2)"},
+            "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tc_peak,
+                         "unit": "TFLOP/s", "frac": achieved_tflops / tc_peak, "traffic": traffic,
+                         "kernel": "stage1_tc_kernel",
+                         "peak_note": "dense fp16/bf16 tensor peak, measured sustained "
+                                      "(MEASURED_PEAKS.json bf16_tflops_sustained); achieved = "
+                                      "ALGORITHMIC fp32-equivalent FLOPs of CNN1 / measured stage-1 time. "
+                                      "The MMAs actually issued are ~8x that (hi+lo splits, implicit-GEMM "
+                                      "zero taps; DESIGN.md K2); ncu: tc pipe 88% busy (operand fetch)",
+                         "fp32_ffma_peak": fp32_peak,
+                         "frac_of_fp32_ffma_peak": achieved_tflops / fp32_peak},
             "e2e": {"value": world * batch * e2e_steps / (ms_e2e / 1000.0), "unit": "frames/s",
                     "h2d_bytes_per_step": int(frames.nbytes), "d2h_bytes_per_step": int(d2h // e2e_steps)},
             "gpu_launches": int(launches),

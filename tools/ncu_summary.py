@@ -14,7 +14,13 @@ for vals in rows[2:]:
             "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
             "smsp__inst_executed.sum", "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum",
             "dram__bytes_read.sum", "dram__bytes_write.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
-            "launch__registers_per_thread", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+            "launch__registers_per_thread", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+            "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+            "l1tex__data_pipe_tc_wavefronts_mem_shared.sum",
+            "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+            "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+            "smsp__sass_inst_executed_op_tmem_ldt.sum", "smsp__sass_inst_executed_op_tmem_stt.sum"]
     for k in keys:
         if k in d: print(f"  {k} = {d[k]} {units[hdr.index(k)]}")
     st = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(v) for k, v in d.items()
