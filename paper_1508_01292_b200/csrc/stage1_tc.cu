@@ -1,5 +1,5 @@
-// stage1_tc.cu -- stage 1 (CNN1 dense scan + threshold + compaction) with layers 1 and 2 on
-// the 5th-generation tensor cores (tcgen05, accumulators in TMEM).  DESIGN.md K2 "v9".
+// stage1_tc.cu -- stage 1 (CNN1 dense scan + threshold + compaction) with the three conv
+// layers on the 5th-generation tensor cores (tcgen05, accumulators in TMEM).  DESIGN.md K2 "v10".
 //
 // PAPER.md §3.3: CNN1 densely scans every pyramid level; its output cells are the 27x31
 // windows at a 4-px step; windows whose response exceeds T1 go to the selective unit.
@@ -8,27 +8,36 @@
 //
 // Work unit: a band of 128 pooled-layer-2 (P2) columns of one level (TW = 123 windows; the
 // patchwork pieces of stage1.cu's plan) x a segment of window rows, marched down one
-// P2 row per step.  Per step:
+// P2 row per step.  Cost model (measured, profiles/r1_tcgen05_probe.jsonl): an MMA costs ~28
+// cycles with A in TMEM and ~40-44 with A in shared memory whatever its N up to ~64, so the
+// design minimises the NUMBER of MMAs and the shared-memory A bytes.  Per step:
 //  * layer 1 = implicit GEMM on the tensor core, A in TMEM: TMEM lane m of tile t holds, per
 //    image row of an 8-row ring, the 8 raw pixels 2x1 .. 2x1+7 (x1 = 128 t + m, exact in
 //    fp16); one MMA (M=128, K=16 = two image rows, N=48 = 2 P1 rows x 4 pool positions x 6
 //    maps) per image-row pair and weight part (w/127.5 * 2^s split into fp16 hi + lo, both
-//    accumulated in fp32): 16 MMAs per step produce two P1 rows of 256 columns, the 2x2 pool
-//    cells of every map in one TMEM lane;
+//    accumulated in fp32): 8 MMAs per tile produce two P1 rows of 128 columns, the 2x2 pool
+//    cells of every map in one TMEM lane.  The two tiles share one 48-column accumulator:
+//    tile 1's MMAs are issued once the data warps have drained tile 0's (mbarrier d1free);
 //  * epilogue (4 warps, one TMEM lane each): max over the pool positions, bias, Eq. 1, split
 //    into fp16 hi + lo, stored as 16-B entries (6 channels + 2 zero) in shared-memory planes,
 //    even / odd columns de-interleaved;
-//  * layer 2 = implicit GEMM from shared memory (no im2col): row m = P2 column X, K = 16 =
-//    (P1 column 2X+2d, 8 channels) + (P1 column 2X+2d+1, 8 channels) -- two core matrices one
-//    plane apart (LBO) -- per kernel row dy; A hi and lo planes, N = 48 = 4 pool positions x 6
-//    maps x {w hi, w lo} (the lo-A x lo-w term dropped: ~2^-22): 16 MMAs per P2 row;
-//  * epilogue: hi + lo halves, max over positions, bias, Eq. 1 -> P2 row (fp32, shared);
-//  * layers 3-4 on the FFMA pipe (as stage1.cu: thread = window column, 6 output rows in
-//    flight, warp-uniform weights from the constant bank), threshold > T1, warp ballot / popc,
-//    one atomicAdd per warp into the survivor queue.
+//  * layer 2 = implicit GEMM from shared memory (no im2col), STREAMED: each P1 row is read
+//    once and feeds the two P2 rows it belongs to -- row m = P2 column X, K = 16 = (P1 column
+//    2X+2d, 8 channels) + (P1 column 2X+2d+1, 8 channels), two core matrices one plane apart
+//    (LBO); N = 96 = {w hi, w lo} x {P2 row q, P2 row q+1} x 4 pool positions x 6 maps for
+//    hi(A), N = 48 (w hi) for lo(A) (lo x lo dropped: ~2^-22): 4 MMAs per P1 row.  The two
+//    accumulators alternate between TMEM halves (B matrices per half parity); a drained half
+//    is zeroed with tcgen05.st before it starts the next P2 row;
+//  * epilogue: hi + lo halves, max over positions, bias, Eq. 1 -> P2 row (fp16 hi / lo);
+//  * layer 3 on tcgen05: row m = window column j, K = 16 = (P2 entry j+kx hi) + (its lo), one
+//    MMA per kx (5), N = 24 = {w hi, w lo} x 6 kernel rows x 2 maps (lo(A) x lo(w) zero): the
+//    contributions of the P2 row to the 6 window rows it reaches; the data warps keep 6 running
+//    sums per map;
+//  * layer 4 (1x1) on the FFMA pipe, threshold > T1, warp ballot / popc, one atomicAdd per
+//    warp into the survivor queue.
 // Warps 0-3 do all data work; warp 4 allocates TMEM and issues every MMA (elect.sync, so the
 // operands stay warp-uniform); MMA completion is tracked with tcgen05.commit -> mbarrier.  The
-// MMAs of layer 1 (two P1 rows ahead) and layer 2 (this row) run while warps 0-3 do layer 3.
+// MMAs of layer 1 (one unit ahead) and layer 2 run while warps 0-3 do the epilogues.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -54,16 +63,17 @@ constexpr int NW = 4;                   // data warps
 constexpr int NT = 32 * (NW + 1);       // + the MMA warp
 constexpr int TW = 123;                 // windows per band (P2 columns 0..126 valid)
 // shared memory (bytes)
-constexpr int B1_BYTES = 8 * 48 * 16 * 2;      // layer-1 B: [pair 4][w part 2] x (48 x 16 fp16)
-constexpr int B2_BYTES = 16 * 48 * 16 * 2;     // layer-2 B: [dy 4][d 2][A part 2]
-constexpr int BMAT = 48 * 16 * 2;              // one B matrix (1536 B): [k chunk 2][n 48][8]
+constexpr int BMAT = 48 * 16 * 2;              // one layer-1 B (N = 48, K = 16): [k chunk 2][n 48][8]
+constexpr int B1_BYTES = 8 * BMAT;             // layer-1 B: [pair 4][w part 2]
+constexpr int BMAT2 = 96 * 16 * 2;             // one layer-2 B (N = 96): [k chunk 2][n 96][8]
+constexpr int B2_BYTES = 8 * BMAT2;            // layer-2 B: [half parity 2][P1 row parity 2][d 2]
+constexpr int BMAT3 = 24 * 16 * 2;             // one layer-3 B (N = 24): [k chunk 2][n 24][8]
+constexpr int B3_BYTES = 5 * BMAT3;            // layer-3 B: [kx 5]
 constexpr int PL_E = 132;                      // entries per (row, part, parity); 128 written
 constexpr int PL_PAR = PL_E * 16;              // 2112 B == 64 mod 128: conflict-free stores
 constexpr int PL_HL = 2 * PL_PAR;
 constexpr int PL_SLOT = 2 * PL_HL;
-constexpr int P1_RING = 6;
-constexpr int B3_BYTES = 6 * 24 * 16 * 2;      // layer-3 B: [kx pair 3][A part 2] x (24 x 16 fp16)
-constexpr int BMAT3 = 24 * 16 * 2;             // [k chunk 2][n 24][8]
+constexpr int P1_RING = 4;                     // P1 rows 2q .. 2q+3 live (layer 2 streams them)
 constexpr int P2_E = 136;                      // P2 entries per (buffer, part): 128 written + reach
 constexpr int P2_HL = P2_E * 16;
 constexpr int P2_BUF = 2 * P2_HL;
@@ -71,18 +81,17 @@ constexpr int OFF_B1 = 0, OFF_B2 = OFF_B1 + B1_BYTES, OFF_B3 = OFF_B2 + B2_BYTES
 constexpr int OFF_PL = OFF_B3 + B3_BYTES;
 constexpr int OFF_P2 = OFF_PL + P1_RING * PL_SLOT;
 constexpr int SMEM_BYTES = OFF_P2 + 2 * P2_BUF;
+static_assert((B1_BYTES + B2_BYTES + B3_BYTES) / 2 == kStage1TcBmatHalves, "B matrix image size");
 // TMEM columns
 constexpr uint32_t TM_A = 0;                   // A ring: tile t at 32 t, image row slot s at +4 s
-constexpr uint32_t TM_D1 = 64;                 // layer-1 accumulators: tile t at 64 + 48 t
-constexpr uint32_t TM_D2 = 160;                // layer-2 accumulator (48)
+constexpr uint32_t TM_D1 = 64;                 // layer-1 accumulator (48), tile 0 then tile 1
+constexpr uint32_t TM_D2 = 112;                // layer-2 accumulators: [half 0 wh | half 1 wh | half 0 wl | half 1 wl]
 constexpr uint32_t TM_D3 = 208;                // layer-3 accumulator (24)
 constexpr uint32_t TM_COLS = 256;
 constexpr uint32_t IDESC = tc05::idesc_f16(128, 48);
+constexpr uint32_t IDESC2 = tc05::idesc_f16(128, 96);
+constexpr uint32_t IDESC2_LO = tc05::idesc_f16(128, 48);    // lo(A): the w-hi columns only
 constexpr uint32_t IDESC3 = tc05::idesc_f16(128, 24);
-// lo(A) parts multiply only the w-hi columns: N = 24 (layer 2), 16 (layer 3: 12 used), same B
-// matrices (their k-chunk stride stays the full width)
-constexpr uint32_t IDESC_LO = tc05::idesc_f16(128, 24);
-constexpr uint32_t IDESC3_LO = tc05::idesc_f16(128, 16);
 
 __device__ __forceinline__ uint32_t h2_of(uint32_t word, uint32_t sel)
 {
@@ -95,21 +104,6 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b)
 {
     const __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<const uint32_t*>(&h);
-}
-__device__ __forceinline__ void ld24(uint32_t taddr, float (&v)[24])
-{
-    uint32_t r[24];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%24];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%25];\n\t"
-        "tcgen05.wait::ld.sync.aligned;"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23])
-        : "r"(taddr), "r"(taddr + 16u)
-        : "memory");
-#pragma unroll
-    for (int i = 0; i < 24; ++i) v[i] = __uint_as_float(r[i]);
 }
 // fp32 pair -> fp16 hi pair + fp16 lo pair (v - hi), packed
 __device__ __forceinline__ void split_h2(float a, float b, uint32_t& hi, uint32_t& lo)
@@ -139,6 +133,19 @@ __device__ __forceinline__ void ld48(uint32_t taddr, float (&v)[48])
     for (int i = 0; i < 48; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// TMEM store of 24 zero columns (32 lanes of the warp's quadrant)
+__device__ __forceinline__ void st_zero24(uint32_t taddr)
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%2,%2,%2,%2,%2,%2,%2,%2,%2,%2,%2,%2,%2,%2,%2,%2};\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%1], {%2,%2,%2,%2,%2,%2,%2,%2};"
+        :: "r"(taddr), "r"(taddr + 16u), "r"(0u) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(tc05::smem_u32(mbar)) : "memory");
+}
+
 template <bool DEBUG>
 __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     const __grid_constant__ Cnn1W W, const float T1, const uint16_t* __restrict__ bmats,
@@ -150,7 +157,7 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ int s_task;
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) uint64_t bar_l1, bar_l2, bar_l3;
+    __shared__ __align__(8) uint64_t bar_l1a, bar_l1b, bar_l2, bar_l3, bar_d1free;
 
     const int tid = threadIdx.x;
     // warp index through shfl: provably warp-uniform, so role branches stay on the uniform
@@ -169,9 +176,11 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     }
     if (mma_warp) tc05::tmem_alloc(&s_tmem, TM_COLS);
     if (tid == 0) {
-        tc05::mbar_init(&bar_l1, 1);
+        tc05::mbar_init(&bar_l1a, 1);
+        tc05::mbar_init(&bar_l1b, 1);
         tc05::mbar_init(&bar_l2, 1);
         tc05::mbar_init(&bar_l3, 1);
+        tc05::mbar_init(&bar_d1free, 32 * NW);
         tc05::mbar_fence_init();
     }
     tc05::fence_async_smem();
@@ -179,7 +188,8 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     __syncthreads();
     tc05::fence_after();
     const uint32_t tm = s_tmem;
-    uint32_t ph_l1 = 0, ph_l2 = 0, ph_l3 = 0;   // completed phases of each mbarrier
+    // completed phases of each mbarrier (the waiting side's count)
+    uint32_t ph_l1a = 0, ph_l1b = 0, ph_l2 = 0, ph_l3 = 0, ph_d1 = 0;
 
     const uint32_t s_base = tc05::smem_u32(smem);
     const int m = 32 * (warp & 3) + lane;    // TMEM lane / P2 column / window column
@@ -241,49 +251,56 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                               h2_of(v1, 0x4140), h2_of(v1, 0x4342));
                 }
             };
-            // layer-1 epilogue of unit k: P1 rows 2k, 2k+1 (task-relative) of both tiles -> planes
-            auto l1_epilogue = [&](int k) {
-#pragma unroll 1
-                for (int t = 0; t < 2; ++t) {
-                    float d[48];
-                    ld48(tm + t_lane + TM_D1 + 48 * t, d);
-                    const int x1 = 128 * t + m;
+            // layer-1 epilogue of unit k, tile t: P1 rows 2k, 2k+1 (task-relative) -> planes;
+            // then release the accumulator to the MMA warp (tile 0 -> tile 1's MMAs)
+            auto l1_epilogue = [&](int k, int t) {
+                float d[48];
+                ld48(tm + t_lane + TM_D1, d);
+                if (t == 0) {
+                    tc05::fence_before();
+                    mbar_arrive(&bar_d1free);
+                }
+                const int x1 = 128 * t + m;
 #pragma unroll
-                    for (int rr = 0; rr < 2; ++rr) {
-                        float v[6];
+                for (int rr = 0; rr < 2; ++rr) {
+                    float v[6];
 #pragma unroll
-                        for (int o = 0; o < 6; ++o) {
-                            const float* q = d + rr * 24 + o;
-                            const float mx = fmaxf(fmaxf(q[0], q[6]), fmaxf(q[12], q[18]));
-                            v[o] = act(fmaf(mx, W.l1_inv_scale, W.b1h[o]));
-                        }
-                        uint32_t hi[3], lo[3];
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) split_h2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
-                        const int slot = (2 * k + rr) % P1_RING;
-                        uint8_t* e = smem + OFF_PL + slot * PL_SLOT + (x1 & 1) * PL_PAR + (x1 >> 1) * 16;
-                        *reinterpret_cast<uint4*>(e) = make_uint4(hi[0], hi[1], hi[2], 0u);
-                        *reinterpret_cast<uint4*>(e + PL_HL) = make_uint4(lo[0], lo[1], lo[2], 0u);
+                    for (int o = 0; o < 6; ++o) {
+                        const float* q = d + rr * 24 + o;
+                        const float mx = fmaxf(fmaxf(q[0], q[6]), fmaxf(q[12], q[18]));
+                        v[o] = act(fmaf(mx, W.l1_inv_scale, W.b1h[o]));
                     }
+                    uint32_t hi[3], lo[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) split_h2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
+                    const int slot = (2 * k + rr) % P1_RING;
+                    uint8_t* e = smem + OFF_PL + slot * PL_SLOT + (x1 & 1) * PL_PAR + (x1 >> 1) * 16;
+                    *reinterpret_cast<uint4*>(e) = make_uint4(hi[0], hi[1], hi[2], 0u);
+                    *reinterpret_cast<uint4*>(e + PL_HL) = make_uint4(lo[0], lo[1], lo[2], 0u);
                 }
             };
-            // layer-2 epilogue: P2 row -> P2 buffer b as fp16 hi / lo entries (column m)
-            auto l2_epilogue = [&](int b) {
-                float d[48];
-                ld48(tm + t_lane + TM_D2, d);
+            // layer-2 epilogue of P2 row q (TMEM half q & 1) -> P2 buffer q & 1 as fp16 hi / lo
+            // entries (column m); the half is zeroed for P2 row q + 2
+            auto l2_epilogue = [&](int q) {
+                const uint32_t h = (uint32_t)(q & 1);
+                float dh[24], dl[24];
+                tc05::ld24(tm + t_lane + TM_D2 + 24 * h, dh);
+                tc05::ld24(tm + t_lane + TM_D2 + 48 + 24 * h, dl);
+                st_zero24(tm + t_lane + TM_D2 + 24 * h);
+                st_zero24(tm + t_lane + TM_D2 + 48 + 24 * h);
                 float v[6];
 #pragma unroll
                 for (int o = 0; o < 6; ++o) {
                     float s4[4];
 #pragma unroll
-                    for (int p = 0; p < 4; ++p) s4[p] = d[p * 6 + o] + d[24 + p * 6 + o];
+                    for (int p = 0; p < 4; ++p) s4[p] = dh[p * 6 + o] + dl[p * 6 + o];
                     const float mx = fmaxf(fmaxf(s4[0], s4[1]), fmaxf(s4[2], s4[3]));
                     v[o] = act(fmaf(mx, W.l2_inv_scale, W.b2[o]));
                 }
                 uint32_t hi[3], lo[3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) split_h2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
-                uint8_t* e = smem + OFF_P2 + b * P2_BUF + m * 16;
+                uint8_t* e = smem + OFF_P2 + (q & 1) * P2_BUF + m * 16;
                 *reinterpret_cast<uint4*>(e) = make_uint4(hi[0], hi[1], hi[2], 0u);
                 *reinterpret_cast<uint4*>(e + P2_HL) = make_uint4(lo[0], lo[1], lo[2], 0u);
             };
@@ -306,7 +323,7 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
             // (TMEM column (w part) * 12 + ky * 2 + mm), then the finished window row p - 5
             auto l3_epilogue = [&](int p) {
                 float d[24];
-                ld24(tm + t_lane + TM_D3, d);
+                tc05::ld24(tm + t_lane + TM_D3, d);
 #pragma unroll
                 for (int i = 0; i < 6; ++i)
 #pragma unroll
@@ -353,8 +370,14 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 tc05::fence_before();
                 __syncthreads();
             };
+            auto wait_l1 = [&](int t) {
+                if (t == 0) { tc05::mbar_wait(&bar_l1a, ph_l1a & 1); ++ph_l1a; }
+                else { tc05::mbar_wait(&bar_l1b, ph_l1b & 1); ++ph_l1b; }
+                tc05::fence_after();
+            };
 
-            // prologue: image rows 0..7 (unit 0), then rows 8..11 once unit 0 is consumed
+            // prologue: image rows 0..7 -> L1(0); rows 8..11 once unit 0 is drained; both
+            // layer-2 halves zeroed before the first streamed MMAs
             {
                 uint32_t wv[8][2];
 #pragma unroll
@@ -366,16 +389,21 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 uint32_t wx[4][2];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) fetch(8 + r, wx[r]);
-                tc05::mbar_wait(&bar_l1, ph_l1 & 1); ++ph_l1;
-                tc05::fence_after();
-                l1_epilogue(0);
+                wait_l1(0);
+                l1_epilogue(0, 0);
+                wait_l1(1);
+                l1_epilogue(0, 1);
+                st_zero24(tm + t_lane + TM_D2);
+                st_zero24(tm + t_lane + TM_D2 + 24);
+                st_zero24(tm + t_lane + TM_D2 + 48);
+                st_zero24(tm + t_lane + TM_D2 + 72);
 #pragma unroll
                 for (int r = 0; r < 4; ++r) put(8 + r, wx[r]);
                 tc05::st_wait();
-                sync_for_mma();                                // -> L1(1)
+                sync_for_mma();                                // -> L1(1), L2s(0)
             }
-            // step q: consume L3(q-2), L1(q+1), L2(q-1) (issue order: the heavy L2 last); the MMA
-            // warp then issues L3(q-1), L1(q+2), L2(q)
+            // iteration q: drain L3(q-2), L1(q+1) tile 0, L2s(q) (-> P2 row q-1, half zeroed),
+            // L1(q+1) tile 1; the MMA warp then issues L3(q-1), L1(q+2), L2s(q+1)
 #pragma unroll 1
             for (int q = 0; q <= NQ + 1; ++q) {
                 const bool more = q + 2 <= NQ;                 // unit q+2 exists
@@ -390,92 +418,108 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                     l3_epilogue(q - 2);
                 }
                 if (q + 1 <= NQ) {
-                    tc05::mbar_wait(&bar_l1, ph_l1 & 1); ++ph_l1;      // L1(q+1) done
-                    tc05::fence_after();
-                    l1_epilogue(q + 1);
+                    wait_l1(0);
+                    l1_epilogue(q + 1, 0);
                 }
-                if (q >= 1 && q <= NQ) {
-                    tc05::mbar_wait(&bar_l2, ph_l2 & 1); ++ph_l2;      // L2(q-1) done
+                if (q <= NQ) {
+                    tc05::mbar_wait(&bar_l2, ph_l2 & 1); ++ph_l2;      // L2s(q) done
                     tc05::fence_after();
-                    l2_epilogue((q - 1) & 1);
+                    if (q >= 1) {
+                        l2_epilogue(q - 1);
+                    } else {                                   // half 1 took unit 0's dy 2, 3 junk
+                        st_zero24(tm + t_lane + TM_D2 + 24);
+                        st_zero24(tm + t_lane + TM_D2 + 72);
+                    }
+                }
+                if (q + 1 <= NQ) {
+                    wait_l1(1);
+                    l1_epilogue(q + 1, 1);
                 }
                 if (more) {
 #pragma unroll
                     for (int r = 0; r < 4; ++r) put(4 * q + 12 + r, wx[r]);
                 }
                 tc05::st_wait();
-                sync_for_mma();                                // -> L1(q+2), L2(q), L3(q-1)
+                sync_for_mma();                                // -> L3(q-1), L1(q+2), L2s(q+1)
             }
         } else {
             // ============================ MMA warp ============================
             const uint64_t bd1 = tc05::sdesc(s_base + OFF_B1, 48 * 16, 128);
-            const uint64_t bd2 = tc05::sdesc(s_base + OFF_B2, 48 * 16, 128);
+            const uint64_t bd2 = tc05::sdesc(s_base + OFF_B2, 96 * 16, 128);
             const uint64_t ad2 = tc05::sdesc(s_base + OFF_PL, PL_PAR, 128);
             const uint64_t bd3 = tc05::sdesc(s_base + OFF_B3, 24 * 16, 128);
-            const uint64_t ad3 = tc05::sdesc(s_base + OFF_P2, 16, 128);
-            auto issue_l1 = [&](int k) {
+            const uint64_t ad3 = tc05::sdesc(s_base + OFF_P2, P2_HL, 128);
+            // layer 1 of unit k, tile t, into the shared accumulator
+            auto issue_l1 = [&](int k, int t) {
                 if (tc05::elect_one()) {
 #pragma unroll
-                    for (int t = 0; t < 2; ++t)
+                    for (int p = 0; p < 4; ++p)
 #pragma unroll
-                        for (int p = 0; p < 4; ++p)
-#pragma unroll
-                            for (int hl = 0; hl < 2; ++hl) {
-                                const uint32_t a = tm + TM_A + 32 * t + 4 * ((4 * k + 2 * p) & 7);
-                                tc05::mma_f16_ts(tm + TM_D1 + 48 * t, a, bd1 + (uint64_t)((p * 2 + hl) * (BMAT >> 4)),
-                                                 IDESC, (p | hl) != 0);
-                            }
-                    tc05::commit(&bar_l1);
+                        for (int hl = 0; hl < 2; ++hl) {
+                            const uint32_t a = tm + TM_A + 32 * t + 4 * ((4 * k + 2 * p) & 7);
+                            tc05::mma_f16_ts(tm + TM_D1, a, bd1 + (uint64_t)((p * 2 + hl) * (BMAT >> 4)),
+                                             IDESC, (p | hl) != 0);
+                        }
+                    tc05::commit(t == 0 ? &bar_l1a : &bar_l1b);
                 }
                 __syncwarp();
             };
-            auto issue_l2 = [&](int q) {
+            auto issue_l1b = [&](int k) {                      // once tile 0 has been drained
+                tc05::mbar_wait(&bar_d1free, ph_d1 & 1); ++ph_d1;
+                tc05::fence_after();
+                issue_l1(k, 1);
+            };
+            // layer 2, streamed: the P1 rows of unit u (2u, 2u+1) into P2 row u-1 (kernel rows
+            // dy 2, 3; TMEM half (u-1) & 1) and P2 row u (dy 0, 1; half u & 1)
+            auto issue_l2s = [&](int u) {
                 if (tc05::elect_one()) {
+                    const int par = (u - 1) & 1;               // half of P2 row u-1
 #pragma unroll
-                    for (int dy = 0; dy < 4; ++dy) {
-                        const uint32_t slot_off = (uint32_t)(((2 * q + dy) % P1_RING) * PL_SLOT);
+                    for (int rp = 0; rp < 2; ++rp) {
+                        const uint32_t slot_off = (uint32_t)(((2 * u + rp) % P1_RING) * PL_SLOT);
 #pragma unroll
-                        for (int d = 0; d < 2; ++d)
-#pragma unroll
-                            for (int ha = 0; ha < 2; ++ha) {
-                                const uint64_t a = ad2 + (uint64_t)((slot_off + ha * PL_HL + d * 16) >> 4);
-                                const uint64_t b = bd2 + (uint64_t)(((dy * 2 + d) * 2 + ha) * (BMAT >> 4));
-                                tc05::mma_f16(tm + TM_D2, a, b, ha ? IDESC_LO : IDESC, (dy | d | ha) != 0);
-                            }
+                        for (int d = 0; d < 2; ++d) {
+                            const uint64_t b = bd2 + (uint64_t)((((par * 2 + rp) * 2 + d) * BMAT2) >> 4);
+                            const uint64_t a = ad2 + (uint64_t)((slot_off + d * 16) >> 4);
+                            tc05::mma_f16(tm + TM_D2, a, b, IDESC2, 1u);
+                            tc05::mma_f16(tm + TM_D2, a + (uint64_t)(PL_HL >> 4), b, IDESC2_LO, 1u);
+                        }
                     }
                     tc05::commit(&bar_l2);
                 }
                 __syncwarp();
             };
-            // layer 3 of P2 row p: row m = window column j, K = 16 = P2 entries j+kx, j+kx+1
-            // (LBO = one entry), N = 24 = {w hi, w lo} x 6 kernel rows x 2 maps
+            // layer 3 of P2 row p: row m = window column j, K = 16 = P2 entry j+kx hi + lo
+            // (LBO = the hi -> lo plane distance), N = 24 = {w hi, w lo} x 6 kernel rows x 2 maps
             auto issue_l3 = [&](int p) {
                 if (tc05::elect_one()) {
 #pragma unroll
-                    for (int kp = 0; kp < 3; ++kp)
-#pragma unroll
-                        for (int ha = 0; ha < 2; ++ha) {
-                            const uint64_t a = ad3 + (uint64_t)(((p & 1) * P2_BUF + ha * P2_HL + kp * 32) >> 4);
-                            const uint64_t b = bd3 + (uint64_t)((kp * 2 + ha) * (BMAT3 >> 4));
-                            tc05::mma_f16(tm + TM_D3, a, b, ha ? IDESC3_LO : IDESC3, (kp | ha) != 0);
-                        }
+                    for (int kx = 0; kx < 5; ++kx) {
+                        const uint64_t a = ad3 + (uint64_t)(((p & 1) * P2_BUF + kx * 16) >> 4);
+                        const uint64_t b = bd3 + (uint64_t)((kx * BMAT3) >> 4);
+                        tc05::mma_f16(tm + TM_D3, a, b, IDESC3, kx != 0);
+                    }
                     tc05::commit(&bar_l3);
                 }
                 __syncwarp();
             };
             __syncthreads();                                   // rows 0..7 in TMEM
             tc05::fence_after();
-            issue_l1(0);
-            __syncthreads();                                   // rows 8..11, P1 rows 0, 1
+            issue_l1(0, 0);
+            issue_l1b(0);
+            __syncthreads();                                   // rows 8..11, P1 rows 0, 1, D2 zeroed
             tc05::fence_after();
-            issue_l1(1);
+            issue_l1(1, 0);
+            issue_l2s(0);
+            issue_l1b(1);
 #pragma unroll 1
             for (int q = 0; q <= NQ + 1; ++q) {
                 __syncthreads();
                 tc05::fence_after();
                 if (q >= 1 && q <= NQ) issue_l3(q - 1);
-                if (q + 2 <= NQ) issue_l1(q + 2);
-                if (q < NQ) issue_l2(q);
+                if (q + 2 <= NQ) issue_l1(q + 2, 0);
+                if (q + 1 <= NQ) issue_l2s(q + 1);
+                if (q + 2 <= NQ) issue_l1b(q + 2);
             }
         }
     }
@@ -512,15 +556,20 @@ int stage1_tc_band_width() { return TW; }
 int stage1_tc_grid(int sm_count) { return sm_count * std::min(occupancy<false>(), occupancy<true>()); }
 int stage1_tc_task_cost(int nrows) { return nrows + 5 + 2; }
 
-// B matrices of both tensor-core layers (fp16 bit patterns, the kernel's shared-memory image);
-// returns the fp16 count.  K-major canonical layout of one B (N = 48, K = 16): [k chunk][n][8].
+// B matrices of the three tensor-core layers (fp16 bit patterns, the kernel's shared-memory
+// image); returns the fp16 count.  K-major canonical layout of one B (N rows, K = 16):
+// [k chunk 2][n N][8].
 int stage1_tc_bmats(const Cnn1W& w, uint16_t* out)
 {
-    auto put = [&](int mat, int n, int kk, float v) {
-        out[mat * (BMAT / 2) + (kk >> 3) * 48 * 8 + n * 8 + (kk & 7)] = __half_as_ushort(__float2half_rn(v));
+    const int total = (B1_BYTES + B2_BYTES + B3_BYTES) / 2;
+    std::fill(out, out + total, (uint16_t)0);
+    auto put = [&](uint16_t* mat, int N, int n, int kk, float v) {
+        mat[(kk >> 3) * N * 8 + n * 8 + (kk & 7)] = __half_as_ushort(__float2half_rn(v));
     };
-    const int total = (B1_BYTES + B2_BYTES) / 2;
-    std::fill(out, out + total + B3_BYTES / 2, (uint16_t)0);
+    auto split = [](float wp, int part) {
+        const float hi = __half2float(__float2half_rn(wp));
+        return part ? wp - hi : wp;
+    };
     // layer 1: mat = pair p * 2 + part; n = rr * 24 + pos * 6 + o; kk = e * 8 + c
     const double sc1 = 1.0 / (double)w.l1_inv_scale;
     for (int p = 0; p < 4; ++p)
@@ -534,49 +583,46 @@ int stage1_tc_bmats(const Cnn1W& w, uint16_t* out)
                             const int ky = d - 2 * rr - py, kx = c - px;
                             if (ky < 0 || ky > 3 || kx < 0 || kx > 3) continue;
                             const float wp = (float)((double)w.w1[o][ky * 4 + kx] / 127.5 * sc1);
-                            const float hi = __half2float(__float2half_rn(wp));
-                            put(p * 2 + part, rr * 24 + pos * 6 + o, kk, part ? wp - hi : wp);
+                            put(out + (p * 2 + part) * (BMAT / 2), 48, rr * 24 + pos * 6 + o, kk, split(wp, part));
                         }
-    // layer 2: mat = 8 + (dy * 2 + d) * 2 + A part; n = w part * 24 + pos * 6 + o; kk = c * 8 + ch
+    // layer 2 (streamed): mat = (par * 2 + rp) * 2 + d, for P1 row 2u + rp of unit u with
+    // P2 row u-1 in TMEM half par (kernel row dy = 2 + rp) and P2 row u in half 1 - par
+    // (dy = rp); n = wpart * 48 + half * 24 + pos * 6 + o; kk = c * 8 + ch, P1 column 2X+2d+c
+    uint16_t* out2 = out + B1_BYTES / 2;
     const double sc2 = 1.0 / (double)w.l2_inv_scale;
-    for (int dy = 0; dy < 4; ++dy)
-        for (int d = 0; d < 2; ++d)
-            for (int ha = 0; ha < 2; ++ha)
-                for (int wh = 0; wh < 2; ++wh) {
-                    if (ha && wh) continue;                 // lo(A) x lo(w) dropped
-                    for (int pos = 0; pos < 4; ++pos)
-                        for (int o = 0; o < 6; ++o)
-                            for (int kk = 0; kk < 16; ++kk) {
-                                const int py = pos >> 1, px = pos & 1;
-                                const int dx = 2 * d + (kk >> 3), ch = kk & 7;
-                                const int ky = dy - py, kx = dx - px;
-                                if (ch >= 6 || ky < 0 || ky > 2 || kx < 0 || kx > 2) continue;
-                                const float wp = (float)((double)w.w2[o][ch][ky * 3 + kx] * sc2);
-                                const float hi = __half2float(__float2half_rn(wp));
-                                put(8 + (dy * 2 + d) * 2 + ha, wh * 24 + pos * 6 + o, kk, wh ? wp - hi : wp);
-                            }
-                }
-    // layer 3: mat = 24 * 2 (B1 + B2 in BMAT units) then [kx pair kp 3][A part 2] (BMAT3 each);
-    // n = w part * 12 + ky * 2 + mm; kk = c * 8 + ch, kx = 2 kp + c
+    for (int par = 0; par < 2; ++par)
+        for (int rp = 0; rp < 2; ++rp)
+            for (int d = 0; d < 2; ++d)
+                for (int wh = 0; wh < 2; ++wh)
+                    for (int half = 0; half < 2; ++half) {
+                        const int dy = half == par ? 2 + rp : rp;
+                        for (int pos = 0; pos < 4; ++pos)
+                            for (int o = 0; o < 6; ++o)
+                                for (int kk = 0; kk < 16; ++kk) {
+                                    const int py = pos >> 1, px = pos & 1;
+                                    const int dx = 2 * d + (kk >> 3), ch = kk & 7;
+                                    const int ky = dy - py, kx = dx - px;
+                                    if (ch >= 6 || ky < 0 || ky > 2 || kx < 0 || kx > 2) continue;
+                                    const float wp = (float)((double)w.w2[o][ch][ky * 3 + kx] * sc2);
+                                    put(out2 + ((par * 2 + rp) * 2 + d) * (BMAT2 / 2), 96,
+                                        wh * 48 + half * 24 + pos * 6 + o, kk, split(wp, wh));
+                                }
+                    }
+    // layer 3: mat = kx; n = wpart * 12 + ky * 2 + mm; kk = A part * 8 + ch (A part 0 = the
+    // P2 entry's hi, 1 = its lo; lo(A) x lo(w) stays zero)
     uint16_t* out3 = out + (B1_BYTES + B2_BYTES) / 2;
     const double sc3 = 1.0 / (double)w.l3_inv_scale;
-    for (int kp = 0; kp < 3; ++kp)
-        for (int ha = 0; ha < 2; ++ha)
-            for (int wh = 0; wh < 2; ++wh) {
-                if (ha && wh) continue;
-                for (int ky = 0; ky < 6; ++ky)
-                    for (int mm = 0; mm < 2; ++mm)
-                        for (int kk = 0; kk < 16; ++kk) {
-                            const int kx = 2 * kp + (kk >> 3), ch = kk & 7;
-                            if (kx > 4 || ch >= 6) continue;
-                            const float wp = (float)((double)w.w3[mm][ch][ky * 5 + kx] * sc3);
-                            const float hi = __half2float(__float2half_rn(wp));
-                            const int n = wh * 12 + ky * 2 + mm;
-                            out3[(kp * 2 + ha) * (BMAT3 / 2) + (kk >> 3) * 24 * 8 + n * 8 + (kk & 7)] =
-                                __half_as_ushort(__float2half_rn(wh ? wp - hi : wp));
-                        }
-            }
-    return total + B3_BYTES / 2;
+    for (int kx = 0; kx < 5; ++kx)
+        for (int wh = 0; wh < 2; ++wh)
+            for (int ky = 0; ky < 6; ++ky)
+                for (int mm = 0; mm < 2; ++mm)
+                    for (int kk = 0; kk < 16; ++kk) {
+                        const int ha = kk >> 3, ch = kk & 7;
+                        if (ch >= 6 || (ha && wh)) continue;
+                        const float wp = (float)((double)w.w3[mm][ch][ky * 5 + kx] * sc3);
+                        put(out3 + kx * (BMAT3 / 2), 24, wh * 12 + ky * 2 + mm, kk, split(wp, wh));
+                    }
+    return total;
 }
 
 void launch_stage1_tc(const Cnn1W& w, float T1, const uint16_t* d_bmats, const uint8_t* levels,
