@@ -37,6 +37,10 @@ struct __align__(16) Cnn1W {   // 797 weights + re-arranged copies for the stage
     // hi + lo; the accumulator is scaled back by l2_inv_scale = 2^-s2
     float l2_inv_scale;
     float l3_inv_scale;        // likewise for layer 3 (w3)
+    // stage1_tc.cu epilogue constants with Eq. 1's inner factor 2/3 folded in (the kernel
+    // evaluates Eq. 1 on x' = 2x/3): [0..5] b1h, [6..11] b2, [12..13] b3, [14] l1_inv_scale,
+    // [15] l2_inv_scale, [16] l3_inv_scale, [17..18] w4, [19] b4, all x 2/3
+    float tcx[20];
 };
 template <int A, int B, int C>
 struct __align__(16) SelNetW { // CNN2: <16,6,2>, CNN3: <2,2,25>

@@ -230,6 +230,17 @@ void unpack_cnn1(const float* w, Cnn1W& o)
         const int e3 = m3 > 0.0 ? (int)std::floor(std::log2(m3)) : 0;
         o.l3_inv_scale = (float)std::ldexp(1.0, e3 - 3);
     }
+    {                                                // stage1_tc.cu epilogues: x' = 2x/3
+        const double k = 2.0 / 3.0;
+        for (int m = 0; m < 6; ++m) o.tcx[m] = (float)(k * (double)o.b1h[m]);
+        for (int m = 0; m < 6; ++m) o.tcx[6 + m] = (float)(k * (double)o.b2[m]);
+        for (int m = 0; m < 2; ++m) o.tcx[12 + m] = (float)(k * (double)o.b3[m]);
+        o.tcx[14] = (float)(k * (double)o.l1_inv_scale);
+        o.tcx[15] = (float)(k * (double)o.l2_inv_scale);
+        o.tcx[16] = (float)(k * (double)o.l3_inv_scale);
+        for (int m = 0; m < 2; ++m) o.tcx[17 + m] = (float)(k * (double)o.w4[m]);
+        o.tcx[19] = (float)(k * (double)o.b4);
+    }
     for (int ci = 0; ci < 6; ++ci) {                 // vector-friendly copies (stage1.cu)
         for (int k = 0; k < 56; ++k) o.w2v[ci][k] = k < 54 ? o.w2[k / 9][ci][k % 9] : 0.f;
         for (int i = 0; i < 6; ++i)

@@ -49,11 +49,23 @@
 namespace ccnn {
 namespace {
 
-__device__ __forceinline__ float act(float x)
+// Eq. 1, y = 1.7159 tanh(2x/3) via the paper's approximation, on x' = 2x/3 (the
+// factor is folded into the preceding bias / scale, Cnn1W::tcx), two values per f32x2 op
+__device__ __forceinline__ float2 act2(float2 x)
 {
-    const float a = fabsf(x) * (2.0f / 3.0f);
-    const float a2 = a * a;
-    const float p = fmaf(a2, fmaf(a2, 1.41645f, 1.0f), a + 1.0f);
+    const float2 a2 = __fmul2_rn(x, x);
+    const float2 t = __ffma2_rn(a2, make_float2(1.41645f, 1.41645f), make_float2(1.0f, 1.0f));
+    const float2 p = __ffma2_rn(a2, t, make_float2(fabsf(x.x) + 1.0f, fabsf(x.y) + 1.0f));
+    float2 r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(p.x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(p.y));
+    const float2 y = __ffma2_rn(make_float2(-1.7159f, -1.7159f), r, make_float2(1.7159f, 1.7159f));
+    return make_float2(copysignf(y.x, x.x), copysignf(y.y, x.y));
+}
+__device__ __forceinline__ float act1(float x)           // x' = 2x/3, one value
+{
+    const float a2 = x * x;
+    const float p = fmaf(a2, fmaf(a2, 1.41645f, 1.0f), fabsf(x) + 1.0f);
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(p));
     return copysignf(fmaf(-1.7159f, r, 1.7159f), x);
@@ -106,12 +118,12 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b)
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 // fp32 pair -> fp16 hi pair + fp16 lo pair (v - hi), packed
-__device__ __forceinline__ void split_h2(float a, float b, uint32_t& hi, uint32_t& lo)
+__device__ __forceinline__ void split_h2(float2 v, uint32_t& hi, uint32_t& lo)
 {
-    const __half2 h = __floats2half2_rn(a, b);
-    const float2 hf = __half22float2(h);
+    const __half2 h = __float22half2_rn(v);
+    const float2 d = __ffma2_rn(__half22float2(h), make_float2(-1.0f, -1.0f), v);   // exact
     hi = *reinterpret_cast<const uint32_t*>(&h);
-    lo = pack_h2(a - hf.x, b - hf.y);
+    lo = pack_h2(d.x, d.y);
 }
 __device__ __forceinline__ void ld48(uint32_t taddr, float (&v)[48])
 {
@@ -263,16 +275,19 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 const int x1 = 128 * t + m;
 #pragma unroll
                 for (int rr = 0; rr < 2; ++rr) {
-                    float v[6];
-#pragma unroll
-                    for (int o = 0; o < 6; ++o) {
-                        const float* q = d + rr * 24 + o;
-                        const float mx = fmaxf(fmaxf(q[0], q[6]), fmaxf(q[12], q[18]));
-                        v[o] = act(fmaf(mx, W.l1_inv_scale, W.b1h[o]));
-                    }
                     uint32_t hi[3], lo[3];
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) split_h2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
+                    for (int c = 0; c < 3; ++c) {
+                        float mx[2];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const float* q = d + rr * 24 + 2 * c + e;
+                            mx[e] = fmaxf(fmaxf(q[0], q[6]), fmaxf(q[12], q[18]));
+                        }
+                        const float2 x = __ffma2_rn(make_float2(mx[0], mx[1]), make_float2(W.tcx[14], W.tcx[14]),
+                                                    make_float2(W.tcx[2 * c], W.tcx[2 * c + 1]));
+                        split_h2(act2(x), hi[c], lo[c]);
+                    }
                     const int slot = (2 * k + rr) % P1_RING;
                     uint8_t* e = smem + OFF_PL + slot * PL_SLOT + (x1 & 1) * PL_PAR + (x1 >> 1) * 16;
                     *reinterpret_cast<uint4*>(e) = make_uint4(hi[0], hi[1], hi[2], 0u);
@@ -288,18 +303,20 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 tc05::ld24(tm + t_lane + TM_D2 + 48 + 24 * h, dl);
                 st_zero24(tm + t_lane + TM_D2 + 24 * h);
                 st_zero24(tm + t_lane + TM_D2 + 48 + 24 * h);
-                float v[6];
-#pragma unroll
-                for (int o = 0; o < 6; ++o) {
-                    float s4[4];
-#pragma unroll
-                    for (int p = 0; p < 4; ++p) s4[p] = dh[p * 6 + o] + dl[p * 6 + o];
-                    const float mx = fmaxf(fmaxf(s4[0], s4[1]), fmaxf(s4[2], s4[3]));
-                    v[o] = act(fmaf(mx, W.l2_inv_scale, W.b2[o]));
-                }
                 uint32_t hi[3], lo[3];
 #pragma unroll
-                for (int c = 0; c < 3; ++c) split_h2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
+                for (int c = 0; c < 3; ++c) {
+                    float2 s4[4];
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+                        s4[p] = __fadd2_rn(make_float2(dh[p * 6 + 2 * c], dh[p * 6 + 2 * c + 1]),
+                                           make_float2(dl[p * 6 + 2 * c], dl[p * 6 + 2 * c + 1]));
+                    const float m0 = fmaxf(fmaxf(s4[0].x, s4[1].x), fmaxf(s4[2].x, s4[3].x));
+                    const float m1 = fmaxf(fmaxf(s4[0].y, s4[1].y), fmaxf(s4[2].y, s4[3].y));
+                    const float2 x = __ffma2_rn(make_float2(m0, m1), make_float2(W.tcx[15], W.tcx[15]),
+                                                make_float2(W.tcx[6 + 2 * c], W.tcx[7 + 2 * c]));
+                    split_h2(act2(x), hi[c], lo[c]);
+                }
                 uint8_t* e = smem + OFF_P2 + (q & 1) * P2_BUF + m * 16;
                 *reinterpret_cast<uint4*>(e) = make_uint4(hi[0], hi[1], hi[2], 0u);
                 *reinterpret_cast<uint4*>(e + P2_HL) = make_uint4(lo[0], lo[1], lo[2], 0u);
@@ -325,22 +342,24 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 float d[24];
                 tc05::ld24(tm + t_lane + TM_D3, d);
 #pragma unroll
-                for (int i = 0; i < 6; ++i)
-#pragma unroll
-                    for (int mm = 0; mm < 2; ++mm) {
-                        const int n = (5 - i) * 2 + mm;
-                        acc3[mm][i] += d[n] + d[12 + n];
-                    }
+                for (int i = 0; i < 6; ++i) {
+                    const int n = (5 - i) * 2;
+                    const float2 c2 = __fadd2_rn(make_float2(d[n], d[n + 1]), make_float2(d[12 + n], d[13 + n]));
+                    const float2 a2 = __fadd2_rn(make_float2(acc3[0][i], acc3[1][i]), c2);
+                    acc3[0][i] = a2.x;
+                    acc3[1][i] = a2.y;
+                }
                 const int o = p - 5;                        // finished window row (task-relative)
-                const float a0 = act(fmaf(acc3[0][0], W.l3_inv_scale, W.b3[0]));
-                const float a1 = act(fmaf(acc3[1][0], W.l3_inv_scale, W.b3[1]));
+                const float2 a = act2(__ffma2_rn(make_float2(acc3[0][0], acc3[1][0]),
+                                                 make_float2(W.tcx[16], W.tcx[16]),
+                                                 make_float2(W.tcx[12], W.tcx[13])));
 #pragma unroll
                 for (int mm = 0; mm < 2; ++mm) {
 #pragma unroll
                     for (int i = 0; i < 5; ++i) acc3[mm][i] = acc3[mm][i + 1];
                     acc3[mm][5] = 0.f;
                 }
-                const float score = act(fmaf(W.w4[1], a1, fmaf(W.w4[0], a0, W.b4)));
+                const float score = act1(fmaf(W.tcx[18], a.y, fmaf(W.tcx[17], a.x, W.tcx[19])));
                 const bool valid = (o >= 0) && (o < e_rows) && e_col;
                 if (DEBUG && valid) dbg_map[LE.map_off + (int64_t)(T.y0 + o) * LE.nx + e_x] = score;
                 const bool pred = valid && (score > T1);             // "exceeded"
