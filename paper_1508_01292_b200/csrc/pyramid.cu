@@ -61,8 +61,11 @@ __device__ __forceinline__ void load_rows(const uint32_t* __restrict__ yt, uint3
     }
 }
 
+#ifndef PYR_MINB
+#define PYR_MINB 1
+#endif
 template <bool SAFE>
-__global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
+__global__ void __launch_bounds__(kPyrCols, PYR_MINB) pyramid_kernel(
     const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
     const LevelInfo* __restrict__ lv, const uint32_t* __restrict__ tiles,
     const uint32_t* __restrict__ tabs)
