@@ -96,7 +96,7 @@ struct ccnn_ctx {
     std::vector<uint32_t> ptiles;       // pyramid tile descriptors (pyramid.cu)
 
     // shared by consecutive batches (their kernels are ordered on the compute stream)
-    DevBuf arena, d_levels, d_tasks, d_cta_first, d_tabs, d_ptiles, cands, selout, dbg_resp, acc, staging,
+    DevBuf d_levels, d_tasks, d_cta_first, d_tabs, d_ptiles, cands, selout, dbg_resp, acc, staging,
         counts, dbg_map;
 
     // per in-flight batch (ccnn_submit / ccnn_collect ping-pong, NEXT #2 streaming ingest)
@@ -107,8 +107,10 @@ struct ccnn_ctx {
         GrayJob* h_jobs = nullptr;  // pinned staging of jobs (max_batch entries)
         FrameInfo* h_finfo = nullptr;   // pinned staging of finfo (max_batch entries)
         DevBuf ctrl, out;           // control block, compacted boxes
+        DevBuf arena;               // all levels of the batch (the pyramid of batch k+1 runs on
+                                    // the pyramid stream while batch k's stage 1 reads its own)
         Ctrl* h_ctrl = nullptr;     // pinned readback of ctrl
-        cudaEvent_t ev[7] = {};     // h2d0, h2d1, c0, pyramid, stage1, selective, end
+        cudaEvent_t ev[8] = {};     // h2d0, h2d1, c0, pyramid, stage1, selective, end, stage-1 start
         bool used = false;          // a batch has been enqueued on this slot before
         int n = 0, n_jobs = 0;
         uint32_t cand_cap = 0;
@@ -116,6 +118,9 @@ struct ccnn_ctx {
         bool timed = false, empty = false;
     } slot[2];
     cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
+    cudaStream_t pyr_stream = nullptr;  // pyramids (overlap the previous batch's stage 1..NMS)
+    cudaStream_t comp = nullptr;        // stage 1 .. NMS; ordered after the user's stream
+                                        // (ccnn_set_stream) through the frames-ready event
     int next_slot = 0, inflight = 0;
 
     // texture objects over frames (pyramid tex2Dgather path), keyed by (data, w, h, pitch)
@@ -612,6 +617,13 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
     ctx->tex_pitch_align = std::max(ctx->tex_pitch_align, 1);
     CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+    {   // the compute stream outranks the pyramid stream: when both have CTAs waiting, the
+        // block scheduler places stage 1 .. NMS first and the next batch's pyramid fills in
+        int least = 0, greatest = 0;
+        CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        CU(cudaStreamCreateWithPriority(&ctx->pyr_stream, cudaStreamNonBlocking, least));
+        CU(cudaStreamCreateWithPriority(&ctx->comp, cudaStreamNonBlocking, greatest));
+    }
     *out = ctx;
     return CCNN_OK;
 }
@@ -636,7 +648,7 @@ void ccnn_destroy(ccnn_ctx* ctx)
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     drop_textures(ctx, nullptr, 0);
-    for (DevBuf* b : {&ctx->arena, &ctx->d_levels, &ctx->d_tasks, &ctx->d_cta_first, &ctx->d_tabs, &ctx->d_ptiles,
+    for (DevBuf* b : {&ctx->d_levels, &ctx->d_tasks, &ctx->d_cta_first, &ctx->d_tabs, &ctx->d_ptiles,
                       &ctx->cands, &ctx->selout, &ctx->dbg_resp, &ctx->acc, &ctx->staging, &ctx->counts,
                       &ctx->dbg_map, &ctx->s1_bmats})
         b->release();
@@ -649,11 +661,14 @@ void ccnn_destroy(ccnn_ctx* ctx)
         if (sl.h_jobs) cudaFreeHost(sl.h_jobs);
         sl.ctrl.release();
         sl.out.release();
+        sl.arena.release();
         if (sl.h_ctrl) cudaFreeHost(sl.h_ctrl);
         for (auto& e : sl.ev) if (e) cudaEventDestroy(e);
     }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
+    if (ctx->pyr_stream) cudaStreamDestroy(ctx->pyr_stream);
+    if (ctx->comp) cudaStreamDestroy(ctx->comp);
     delete ctx;
 }
 
@@ -685,11 +700,15 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     }
     if (ctx->inflight >= 2) return fail(ctx, CCNN_E_STATE, "two batches in flight: ccnn_collect first");
     CU(cudaSetDevice(ctx->device));
-    cudaStream_t s = ctx->stream;
+    // device work: pyramid on pyr_stream, the rest on comp; both start after an event recorded
+    // on the user's stream (device frames written there are complete), so batch k+1's pyramid
+    // can overlap batch k's later stages
+    cudaStream_t s = ctx->comp;
 
     const bool replan = !(key == ctx->key);
     if (replan) {
         CU(cudaStreamSynchronize(s));              // tables of an in-flight batch stay valid
+        CU(cudaStreamSynchronize(ctx->pyr_stream));
         build_plan(ctx, key);
     }
     const int L = (int)ctx->levels.size();
@@ -721,7 +740,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
 
     const uint32_t cand_cap = (uint32_t)std::min<int64_t>((int64_t)ctx->queue_cap * n, 0x7FFFFFFF);
     sl.cand_cap = cand_cap;
-    CU(ctx->arena.ensure((size_t)ctx->arena_bytes));
+    CU(sl.arena.ensure((size_t)ctx->arena_bytes));
     CU(ctx->d_levels.ensure(sizeof(LevelInfo) * L));
     CU(ctx->d_tasks.ensure(sizeof(S1Task) * ctx->tasks.size()));
     CU(ctx->d_cta_first.ensure(sizeof(int32_t) * ctx->cta_first.size()));
@@ -800,7 +819,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
                                          gbuf + foff[f], dp, frames[f].w, frames[f].h};
             }
         }
-        cudaStream_t cs = frames_on_device ? s : ctx->copy_stream;
+        cudaStream_t cs = frames_on_device ? ctx->stream : ctx->copy_stream;
         if (!frames_on_device) {
             // the previous batch of this slot (k-2) read these buffers until its end event
             if (sl.used) CU(cudaStreamWaitEvent(ctx->copy_stream, sl.ev[6], 0));
@@ -841,6 +860,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     sl.n_jobs = n_jobs;
     if (ctx->tex_cache.size() > 4096) {                // bounded cache: rebuild
         CU(cudaStreamSynchronize(s));
+        CU(cudaStreamSynchronize(ctx->pyr_stream));
         drop_textures(ctx, nullptr, 0);
     }
     // texture-gather pyramid only on request: measured slower than byte gathers on B200
@@ -854,22 +874,30 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
         fi[f].tex = use_tex ? frame_texture(ctx, fi[f].data, fi[f].w, fi[f].h, fi[f].pitch) : 0;
         use_tex = use_tex && fi[f].tex != 0;
     }
-    CU(cudaMemcpyAsync(sl.finfo.p, fi, sizeof(FrameInfo) * n, cudaMemcpyHostToDevice, s));
+    // pyramid on its own stream: after the frames are in place and after the previous batch
+    // of this slot finished reading the slot's level arena (its stage 1); it overlaps the
+    // previous batch's stage 1 .. NMS on the compute stream
+    cudaStream_t ps = ctx->pyr_stream;
+    CU(cudaStreamWaitEvent(ps, sl.ev[1], 0));
+    if (sl.used) CU(cudaStreamWaitEvent(ps, sl.ev[4], 0));
+    CU(cudaMemcpyAsync(sl.finfo.p, fi, sizeof(FrameInfo) * n, cudaMemcpyHostToDevice, ps));
     const FrameInfo* dfi = sl.finfo.as<FrameInfo>();
+    CU(cudaEventRecord(sl.ev[2], ps));
+    launch_pyramid(dfi, n, ctx->pyr_tiles, ctx->all_safe, use_tex, sl.arena.as<uint8_t>(),
+                   ctx->d_levels.as<LevelInfo>(), ctx->d_ptiles.as<uint32_t>(),
+                   ctx->d_tabs.as<uint32_t>(), ps);
+    CU(cudaEventRecord(sl.ev[3], ps));
     Ctrl* dctrl = sl.ctrl.as<Ctrl>();
     CU(cudaMemsetAsync(dctrl, 0, sizeof(Ctrl), s));
-    CU(cudaEventRecord(sl.ev[2], s));
-    launch_pyramid(dfi, n, ctx->pyr_tiles, ctx->all_safe, use_tex, ctx->arena.as<uint8_t>(),
-                   ctx->d_levels.as<LevelInfo>(), ctx->d_ptiles.as<uint32_t>(),
-                   ctx->d_tabs.as<uint32_t>(), s);
-    CU(cudaEventRecord(sl.ev[3], s));
+    CU(cudaStreamWaitEvent(s, sl.ev[3], 0));
+    CU(cudaEventRecord(sl.ev[7], s));
     if (ctx->s1_tc)
-        launch_stage1_tc(ctx->w1, ctx->T1, ctx->s1_bmats.as<uint16_t>(), ctx->arena.as<uint8_t>(),
+        launch_stage1_tc(ctx->w1, ctx->T1, ctx->s1_bmats.as<uint16_t>(), sl.arena.as<uint8_t>(),
                          ctx->d_levels.as<LevelInfo>(), ctx->d_tasks.as<S1Task>(), ctx->d_cta_first.as<int32_t>(),
                          (int)ctx->cta_first.size() - 1, ctx->cands.as<S1Cand>(), cand_cap, dctrl,
                          dbg1 ? ctx->dbg_map.as<float>() : nullptr, s);
     else
-        launch_stage1(ctx->w1, ctx->T1, ctx->arena.as<uint8_t>(), ctx->d_levels.as<LevelInfo>(),
+        launch_stage1(ctx->w1, ctx->T1, sl.arena.as<uint8_t>(), ctx->d_levels.as<LevelInfo>(),
                       ctx->d_tasks.as<S1Task>(), ctx->d_cta_first.as<int32_t>(),
                       (int)ctx->cta_first.size() - 1, ctx->cands.as<S1Cand>(), cand_cap, dctrl,
                       dbg1 ? ctx->dbg_map.as<float>() : nullptr, s);
@@ -939,7 +967,7 @@ int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_box
         stats->stage3 = hc.n_stage3;
         stats->nms = hc.n_out;
         stats->kernel_launches = 4 + (sl.n_jobs ? 1 : 0);
-        const int from[5] = {0, 2, 3, 4, 5}, to[5] = {1, 3, 4, 5, 6};
+        const int from[5] = {0, 2, 7, 4, 5}, to[5] = {1, 3, 4, 5, 6};
         for (int k = 0; k < 5; ++k) {
             float t = 0.f;
             cudaEventElapsedTime(&t, sl.ev[from[k]], sl.ev[to[k]]);
@@ -1031,7 +1059,7 @@ int ccnn_debug_level(ccnn_ctx* ctx, int frame, int level, uint8_t* out, int64_t 
     if (!L) return fail(ctx, CCNN_E_ARG, "frame/level out of range");
     if (cap < (int64_t)L->lw * L->lh) return fail(ctx, CCNN_E_CAPACITY, "cap < lw*lh");
     CU(cudaSetDevice(ctx->device));
-    CU(cudaMemcpy2DAsync(out, L->lw, ctx->arena.as<uint8_t>() + L->offset, L->pitch, L->lw, L->lh,
+    CU(cudaMemcpy2DAsync(out, L->lw, ctx->slot[ctx->last_slot].arena.as<uint8_t>() + L->offset, L->pitch, L->lw, L->lh,
                          cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return CCNN_OK;
