@@ -170,7 +170,7 @@ int stage1_tc_band_width();
 int stage1_tc_grid(int sm_count);
 int stage1_tc_task_cost(int nrows);
 int stage1_tc_bmats(const Cnn1W& w, uint16_t* out);   // fills out (kStage1TcBmatHalves), returns count
-constexpr int kStage1TcBmatHalves = 8 * 48 * 16 + 8 * 96 * 16 + 5 * 24 * 16;   // layers 1, 2, 3
+constexpr int kStage1TcBmatHalves = 8 * 96 * 16 + 8 * 96 * 16 + 5 * 24 * 16;   // layers 1, 2, 3
 // selective unit (stage 2/3), persistent over the survivor queue
 struct SelParams { float T2a, T2b; int32_t Tnn, rule; };
 void launch_selective(const Cnn2W& w2, const Cnn3W& w3, SelParams sp, const FrameInfo* d_frames,

@@ -54,10 +54,15 @@ __device__ __forceinline__ uint8_t blend(int p00, int p01, int p10, int p11, int
 // runtime.cu build_plan), the same address across the CTA
 __device__ __forceinline__ void load_rows(const uint32_t* __restrict__ yt, uint32_t (&ye)[kPyrRows])
 {
+    if constexpr (kPyrRows % 4 == 0) {
 #pragma unroll
-    for (int k = 0; k < kPyrRows / 4; ++k) {
-        const uint4 a = __ldg(reinterpret_cast<const uint4*>(yt) + k);
-        ye[4 * k + 0] = a.x; ye[4 * k + 1] = a.y; ye[4 * k + 2] = a.z; ye[4 * k + 3] = a.w;
+        for (int k = 0; k < kPyrRows / 4; ++k) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4*>(yt) + k);
+            ye[4 * k + 0] = a.x; ye[4 * k + 1] = a.y; ye[4 * k + 2] = a.z; ye[4 * k + 3] = a.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kPyrRows; ++k) ye[k] = __ldg(yt + k);
     }
 }
 

@@ -11,13 +11,12 @@
 // P2 row per step.  Cost model (measured, profiles/r1_tcgen05_probe.jsonl): an MMA costs ~28
 // cycles with A in TMEM and ~40-44 with A in shared memory whatever its N up to ~64, so the
 // design minimises the NUMBER of MMAs and the shared-memory A bytes.  Per step:
-//  * layer 1 = implicit GEMM on the tensor core, A in TMEM: TMEM lane m of tile t holds, per
-//    image row of an 8-row ring, the 8 raw pixels 2x1 .. 2x1+7 (x1 = 128 t + m, exact in
-//    fp16); one MMA (M=128, K=16 = two image rows, N=48 = 2 P1 rows x 4 pool positions x 6
-//    maps) per image-row pair and weight part (w/127.5 * 2^s split into fp16 hi + lo, both
-//    accumulated in fp32): 8 MMAs per tile produce two P1 rows of 128 columns, the 2x2 pool
-//    cells of every map in one TMEM lane.  The two tiles share one 48-column accumulator:
-//    tile 1's MMAs are issued once the data warps have drained tile 0's (mbarrier d1free);
+//  * layer 1 = implicit GEMM on the tensor core, A in TMEM: TMEM lane m (= P2 column X) holds,
+//    per image row of an 8-row ring, the 8 raw pixels 4X .. 4X+7 (two aligned level words,
+//    exact in fp16); one MMA (M=128, K=16 = two image rows, N=96 = 2 P1 columns (2X, 2X+1) x
+//    2 P1 rows x 4 pool positions x 6 maps) per image-row pair and weight part (w/127.5 * 2^s
+//    split into fp16 hi + lo, both accumulated in fp32): 8 MMAs produce two P1 rows of the
+//    band's 256 columns, the 2x2 pool cells of every map in one TMEM lane;
 //  * epilogue (4 warps, one TMEM lane each): max over the pool positions, bias, Eq. 1, split
 //    into fp16 hi + lo, stored as 16-B entries (6 channels + 2 zero) in shared-memory planes,
 //    even / odd columns de-interleaved;
@@ -75,7 +74,7 @@ constexpr int NW = 4;                   // data warps
 constexpr int NT = 32 * (NW + 1);       // + the MMA warp
 constexpr int TW = 123;                 // windows per band (P2 columns 0..126 valid)
 // shared memory (bytes)
-constexpr int BMAT = 48 * 16 * 2;              // one layer-1 B (N = 48, K = 16): [k chunk 2][n 48][8]
+constexpr int BMAT = 96 * 16 * 2;              // one layer-1 B (N = 96, K = 16): [k chunk 2][n 96][8]
 constexpr int B1_BYTES = 8 * BMAT;             // layer-1 B: [pair 4][w part 2]
 constexpr int BMAT2 = 96 * 16 * 2;             // one layer-2 B (N = 96): [k chunk 2][n 96][8]
 constexpr int B2_BYTES = 8 * BMAT2;            // layer-2 B: [half parity 2][P1 row parity 2][d 2]
@@ -95,12 +94,12 @@ constexpr int OFF_P2 = OFF_PL + P1_RING * PL_SLOT;
 constexpr int SMEM_BYTES = OFF_P2 + 2 * P2_BUF;
 static_assert((B1_BYTES + B2_BYTES + B3_BYTES) / 2 == kStage1TcBmatHalves, "B matrix image size");
 // TMEM columns
-constexpr uint32_t TM_A = 0;                   // A ring: tile t at 32 t, image row slot s at +4 s
-constexpr uint32_t TM_D1 = 64;                 // layer-1 accumulator (48), tile 0 then tile 1
-constexpr uint32_t TM_D2 = 112;                // layer-2 accumulators: [half 0 wh | half 1 wh | half 0 wl | half 1 wl]
-constexpr uint32_t TM_D3 = 208;                // layer-3 accumulator (24)
+constexpr uint32_t TM_A = 0;                   // A ring: image row slot s at +4 s (32 columns)
+constexpr uint32_t TM_D1 = 32;                 // layer-1 accumulator (96)
+constexpr uint32_t TM_D2 = 128;                // layer-2 accumulators: [half 0 wh | half 1 wh | half 0 wl | half 1 wl]
+constexpr uint32_t TM_D3 = 224;                // layer-3 accumulator (24)
 constexpr uint32_t TM_COLS = 256;
-constexpr uint32_t IDESC = tc05::idesc_f16(128, 48);
+constexpr uint32_t IDESC = tc05::idesc_f16(128, 96);
 constexpr uint32_t IDESC2 = tc05::idesc_f16(128, 96);
 constexpr uint32_t IDESC2_LO = tc05::idesc_f16(128, 48);    // lo(A): the w-hi columns only
 constexpr uint32_t IDESC3 = tc05::idesc_f16(128, 24);
@@ -153,10 +152,6 @@ __device__ __forceinline__ void st_zero24(uint32_t taddr)
         "tcgen05.st.sync.aligned.32x32b.x8.b32 [%1], {%2,%2,%2,%2,%2,%2,%2,%2};"
         :: "r"(taddr), "r"(taddr + 16u), "r"(0u) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* mbar)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(tc05::smem_u32(mbar)) : "memory");
-}
 
 template <bool DEBUG>
 __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
@@ -169,7 +164,7 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ int s_task;
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) uint64_t bar_l1a, bar_l1b, bar_l2, bar_l3, bar_d1free;
+    __shared__ __align__(8) uint64_t bar_l1, bar_l2, bar_l3;
 
     const int tid = threadIdx.x;
     // warp index through shfl: provably warp-uniform, so role branches stay on the uniform
@@ -188,11 +183,9 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     }
     if (mma_warp) tc05::tmem_alloc(&s_tmem, TM_COLS);
     if (tid == 0) {
-        tc05::mbar_init(&bar_l1a, 1);
-        tc05::mbar_init(&bar_l1b, 1);
+        tc05::mbar_init(&bar_l1, 1);
         tc05::mbar_init(&bar_l2, 1);
         tc05::mbar_init(&bar_l3, 1);
-        tc05::mbar_init(&bar_d1free, 32 * NW);
         tc05::mbar_fence_init();
     }
     tc05::fence_async_smem();
@@ -201,7 +194,7 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     tc05::fence_after();
     const uint32_t tm = s_tmem;
     // completed phases of each mbarrier (the waiting side's count)
-    uint32_t ph_l1a = 0, ph_l1b = 0, ph_l2 = 0, ph_l3 = 0, ph_d1 = 0;
+    uint32_t ph_l1 = 0, ph_l2 = 0, ph_l3 = 0;
 
     const uint32_t s_base = tc05::smem_u32(smem);
     const int m = 32 * (warp & 3) + lane;    // TMEM lane / P2 column / window column
@@ -241,57 +234,44 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
 
         if (!mma_warp) {
             // ============================ data warps ============================
-            // loader: lane l < 18 of warp w owns band word 64 t + 16 w + l of tile t; lane m
-            // builds its 8 pixels 2x1 .. 2x1+7 from words (m >> 1) + {0, 1, 2} of its warp by shfl
-            const int lw_ = lane < 18 ? lane : 17;
-            const Src ls0 = src_of(16 * warp + lw_);
-            const Src ls1 = src_of(64 + 16 * warp + lw_);
-            const uint32_t psel = (lane & 1) ? 0x5432u : 0x3210u;
-            const int sl0 = lane >> 1;
+            // loader: lane m (P2 column X = m) loads band words X and X+1 (pixels 4X .. 4X+7) of
+            // each image row and writes them as 4 fp16 pairs to its TMEM lane
+            const Src ls0 = src_of(m);
+            const Src ls1 = src_of(m + 1);
             auto fetch = [&](int r, uint32_t (&wv)[2]) {
                 wv[0] = gword(ls0, r);
                 wv[1] = gword(ls1, r);
             };
             auto put = [&](int r, const uint32_t (&wv)[2]) {      // image row r -> ring slot r % 8
-#pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    const uint32_t w0 = __shfl_sync(0xFFFFFFFFu, wv[t], sl0);
-                    const uint32_t w1 = __shfl_sync(0xFFFFFFFFu, wv[t], sl0 + 1);
-                    const uint32_t w2 = __shfl_sync(0xFFFFFFFFu, wv[t], sl0 + 2);
-                    const uint32_t v0 = __byte_perm(w0, w1, psel), v1 = __byte_perm(w1, w2, psel);
-                    tc05::st4(tm + t_lane + TM_A + 32 * t + 4 * (r & 7), h2_of(v0, 0x4140), h2_of(v0, 0x4342),
-                              h2_of(v1, 0x4140), h2_of(v1, 0x4342));
-                }
+                tc05::st4(tm + t_lane + TM_A + 4 * (r & 7), h2_of(wv[0], 0x4140), h2_of(wv[0], 0x4342),
+                          h2_of(wv[1], 0x4140), h2_of(wv[1], 0x4342));
             };
-            // layer-1 epilogue of unit k, tile t: P1 rows 2k, 2k+1 (task-relative) -> planes;
-            // then release the accumulator to the MMA warp (tile 0 -> tile 1's MMAs)
-            auto l1_epilogue = [&](int k, int t) {
-                float d[48];
-                ld48(tm + t_lane + TM_D1, d);
-                if (t == 0) {
-                    tc05::fence_before();
-                    mbar_arrive(&bar_d1free);
-                }
-                const int x1 = 128 * t + m;
+            // layer-1 epilogue of unit k: P1 rows 2k, 2k+1 (task-relative), columns 2X + cx -> planes
+            auto l1_epilogue = [&](int k) {
+#pragma unroll 1
+                for (int cx = 0; cx < 2; ++cx) {
+                    float d[48];
+                    ld48(tm + t_lane + TM_D1 + 48 * cx, d);
 #pragma unroll
-                for (int rr = 0; rr < 2; ++rr) {
-                    uint32_t hi[3], lo[3];
+                    for (int rr = 0; rr < 2; ++rr) {
+                        uint32_t hi[3], lo[3];
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        float mx[2];
+                        for (int c = 0; c < 3; ++c) {
+                            float mx[2];
 #pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const float* q = d + rr * 24 + 2 * c + e;
-                            mx[e] = fmaxf(fmaxf(q[0], q[6]), fmaxf(q[12], q[18]));
+                            for (int e = 0; e < 2; ++e) {
+                                const float* q = d + rr * 24 + 2 * c + e;
+                                mx[e] = fmaxf(fmaxf(q[0], q[6]), fmaxf(q[12], q[18]));
+                            }
+                            const float2 x = __ffma2_rn(make_float2(mx[0], mx[1]), make_float2(W.tcx[14], W.tcx[14]),
+                                                        make_float2(W.tcx[2 * c], W.tcx[2 * c + 1]));
+                            split_h2(act2(x), hi[c], lo[c]);
                         }
-                        const float2 x = __ffma2_rn(make_float2(mx[0], mx[1]), make_float2(W.tcx[14], W.tcx[14]),
-                                                    make_float2(W.tcx[2 * c], W.tcx[2 * c + 1]));
-                        split_h2(act2(x), hi[c], lo[c]);
+                        const int slot = (2 * k + rr) % P1_RING;
+                        uint8_t* e = smem + OFF_PL + slot * PL_SLOT + cx * PL_PAR + m * 16;
+                        *reinterpret_cast<uint4*>(e) = make_uint4(hi[0], hi[1], hi[2], 0u);
+                        *reinterpret_cast<uint4*>(e + PL_HL) = make_uint4(lo[0], lo[1], lo[2], 0u);
                     }
-                    const int slot = (2 * k + rr) % P1_RING;
-                    uint8_t* e = smem + OFF_PL + slot * PL_SLOT + (x1 & 1) * PL_PAR + (x1 >> 1) * 16;
-                    *reinterpret_cast<uint4*>(e) = make_uint4(hi[0], hi[1], hi[2], 0u);
-                    *reinterpret_cast<uint4*>(e + PL_HL) = make_uint4(lo[0], lo[1], lo[2], 0u);
                 }
             };
             // layer-2 epilogue of P2 row q (TMEM half q & 1) -> P2 buffer q & 1 as fp16 hi / lo
@@ -389,9 +369,8 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 tc05::fence_before();
                 __syncthreads();
             };
-            auto wait_l1 = [&](int t) {
-                if (t == 0) { tc05::mbar_wait(&bar_l1a, ph_l1a & 1); ++ph_l1a; }
-                else { tc05::mbar_wait(&bar_l1b, ph_l1b & 1); ++ph_l1b; }
+            auto wait_l1 = [&]() {
+                tc05::mbar_wait(&bar_l1, ph_l1 & 1); ++ph_l1;
                 tc05::fence_after();
             };
 
@@ -408,10 +387,8 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 uint32_t wx[4][2];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) fetch(8 + r, wx[r]);
-                wait_l1(0);
-                l1_epilogue(0, 0);
-                wait_l1(1);
-                l1_epilogue(0, 1);
+                wait_l1();
+                l1_epilogue(0);
                 st_zero24(tm + t_lane + TM_D2);
                 st_zero24(tm + t_lane + TM_D2 + 24);
                 st_zero24(tm + t_lane + TM_D2 + 48);
@@ -421,8 +398,8 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 tc05::st_wait();
                 sync_for_mma();                                // -> L1(1), L2s(0)
             }
-            // iteration q: drain L3(q-2), L1(q+1) tile 0, L2s(q) (-> P2 row q-1, half zeroed),
-            // L1(q+1) tile 1; the MMA warp then issues L3(q-1), L1(q+2), L2s(q+1)
+            // iteration q: drain L3(q-2), L1(q+1), L2s(q) (-> P2 row q-1, half zeroed); the MMA
+            // warp then issues L3(q-1), L1(q+2), L2s(q+1)
 #pragma unroll 1
             for (int q = 0; q <= NQ + 1; ++q) {
                 const bool more = q + 2 <= NQ;                 // unit q+2 exists
@@ -437,8 +414,8 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                     l3_epilogue(q - 2);
                 }
                 if (q + 1 <= NQ) {
-                    wait_l1(0);
-                    l1_epilogue(q + 1, 0);
+                    wait_l1();
+                    l1_epilogue(q + 1);
                 }
                 if (q <= NQ) {
                     tc05::mbar_wait(&bar_l2, ph_l2 & 1); ++ph_l2;      // L2s(q) done
@@ -450,10 +427,6 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                         st_zero24(tm + t_lane + TM_D2 + 72);
                     }
                 }
-                if (q + 1 <= NQ) {
-                    wait_l1(1);
-                    l1_epilogue(q + 1, 1);
-                }
                 if (more) {
 #pragma unroll
                     for (int r = 0; r < 4; ++r) put(4 * q + 12 + r, wx[r]);
@@ -463,30 +436,25 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
             }
         } else {
             // ============================ MMA warp ============================
-            const uint64_t bd1 = tc05::sdesc(s_base + OFF_B1, 48 * 16, 128);
+            const uint64_t bd1 = tc05::sdesc(s_base + OFF_B1, 96 * 16, 128);
             const uint64_t bd2 = tc05::sdesc(s_base + OFF_B2, 96 * 16, 128);
             const uint64_t ad2 = tc05::sdesc(s_base + OFF_PL, PL_PAR, 128);
             const uint64_t bd3 = tc05::sdesc(s_base + OFF_B3, 24 * 16, 128);
             const uint64_t ad3 = tc05::sdesc(s_base + OFF_P2, P2_HL, 128);
-            // layer 1 of unit k, tile t, into the shared accumulator
-            auto issue_l1 = [&](int k, int t) {
+            // layer 1 of unit k
+            auto issue_l1 = [&](int k) {
                 if (tc05::elect_one()) {
 #pragma unroll
                     for (int p = 0; p < 4; ++p)
 #pragma unroll
                         for (int hl = 0; hl < 2; ++hl) {
-                            const uint32_t a = tm + TM_A + 32 * t + 4 * ((4 * k + 2 * p) & 7);
+                            const uint32_t a = tm + TM_A + 4 * ((4 * k + 2 * p) & 7);
                             tc05::mma_f16_ts(tm + TM_D1, a, bd1 + (uint64_t)((p * 2 + hl) * (BMAT >> 4)),
                                              IDESC, (p | hl) != 0);
                         }
-                    tc05::commit(t == 0 ? &bar_l1a : &bar_l1b);
+                    tc05::commit(&bar_l1);
                 }
                 __syncwarp();
-            };
-            auto issue_l1b = [&](int k) {                      // once tile 0 has been drained
-                tc05::mbar_wait(&bar_d1free, ph_d1 & 1); ++ph_d1;
-                tc05::fence_after();
-                issue_l1(k, 1);
             };
             // layer 2, streamed: the P1 rows of unit u (2u, 2u+1) into P2 row u-1 (kernel rows
             // dy 2, 3; TMEM half (u-1) & 1) and P2 row u (dy 0, 1; half u & 1)
@@ -524,21 +492,18 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
             };
             __syncthreads();                                   // rows 0..7 in TMEM
             tc05::fence_after();
-            issue_l1(0, 0);
-            issue_l1b(0);
+            issue_l1(0);
             __syncthreads();                                   // rows 8..11, P1 rows 0, 1, D2 zeroed
             tc05::fence_after();
-            issue_l1(1, 0);
+            issue_l1(1);
             issue_l2s(0);
-            issue_l1b(1);
 #pragma unroll 1
             for (int q = 0; q <= NQ + 1; ++q) {
                 __syncthreads();
                 tc05::fence_after();
                 if (q >= 1 && q <= NQ) issue_l3(q - 1);
-                if (q + 2 <= NQ) issue_l1(q + 2, 0);
+                if (q + 2 <= NQ) issue_l1(q + 2);
                 if (q + 1 <= NQ) issue_l2s(q + 1);
-                if (q + 2 <= NQ) issue_l1b(q + 2);
             }
         }
     }
@@ -589,21 +554,24 @@ int stage1_tc_bmats(const Cnn1W& w, uint16_t* out)
         const float hi = __half2float(__float2half_rn(wp));
         return part ? wp - hi : wp;
     };
-    // layer 1: mat = pair p * 2 + part; n = rr * 24 + pos * 6 + o; kk = e * 8 + c
+    // layer 1: mat = pair p * 2 + part; n = cx * 48 + rr * 24 + pos * 6 + o (P1 column 2X + cx);
+    // kk = e * 8 + c: image row 2p + e of the unit, pixel 4X + c
     const double sc1 = 1.0 / (double)w.l1_inv_scale;
     for (int p = 0; p < 4; ++p)
         for (int part = 0; part < 2; ++part)
-            for (int rr = 0; rr < 2; ++rr)
-                for (int pos = 0; pos < 4; ++pos)
-                    for (int o = 0; o < 6; ++o)
-                        for (int kk = 0; kk < 16; ++kk) {
-                            const int py = pos >> 1, px = pos & 1;
-                            const int d = 2 * p + (kk >> 3), c = kk & 7;
-                            const int ky = d - 2 * rr - py, kx = c - px;
-                            if (ky < 0 || ky > 3 || kx < 0 || kx > 3) continue;
-                            const float wp = (float)((double)w.w1[o][ky * 4 + kx] / 127.5 * sc1);
-                            put(out + (p * 2 + part) * (BMAT / 2), 48, rr * 24 + pos * 6 + o, kk, split(wp, part));
-                        }
+            for (int cx = 0; cx < 2; ++cx)
+                for (int rr = 0; rr < 2; ++rr)
+                    for (int pos = 0; pos < 4; ++pos)
+                        for (int o = 0; o < 6; ++o)
+                            for (int kk = 0; kk < 16; ++kk) {
+                                const int py = pos >> 1, px = pos & 1;
+                                const int d = 2 * p + (kk >> 3), c = kk & 7;
+                                const int ky = d - 2 * rr - py, kx = c - 2 * cx - px;
+                                if (ky < 0 || ky > 3 || kx < 0 || kx > 3) continue;
+                                const float wp = (float)((double)w.w1[o][ky * 4 + kx] / 127.5 * sc1);
+                                put(out + (p * 2 + part) * (BMAT / 2), 96, cx * 48 + rr * 24 + pos * 6 + o, kk,
+                                    split(wp, part));
+                            }
     // layer 2 (streamed): mat = (par * 2 + rp) * 2 + d, for P1 row 2u + rp of unit u with
     // P2 row u-1 in TMEM half par (kernel row dy = 2 + rp) and P2 row u in half 1 - par
     // (dy = rp); n = wpart * 48 + half * 24 + pos * 6 + o; kk = c * 8 + ch, P1 column 2X+2d+c

@@ -257,6 +257,28 @@ def test_streaming_submit_collect(ws):
     assert np.array_equal(got[4], ref[0])
 
 
+def test_streaming_device_frames_overlapped_pyramid(ws):
+    """The bench's path: device-resident batches, two in flight, so batch k+1's pyramid (own
+    stream, own level arena) overlaps batch k's stage 1 .. NMS: results equal the synchronous
+    ccnn_detect of each batch, in order (C4 4K frames, distinct content per batch)."""
+    import torch
+    c = configs.C4
+    T1, T2 = c.thresholds()
+    batches = [torch.from_numpy(c.make_frames(4, seed=configs.FRAME_SEED + 13 * k)).cuda()
+               for k in range(5)]
+    det = make_det(ws, T1, T2, c.Tnn, c.rule, max_batch=4)
+    ref = [det.detect(b, c.min_face, c.scale_step) for b in batches]
+    got = []
+    det.submit(batches[0], c.min_face, c.scale_step)
+    for k in range(1, len(batches)):
+        det.submit(batches[k], c.min_face, c.scale_step)
+        got.append(det.collect())
+    got.append(det.collect())
+    for k in range(len(batches)):
+        assert np.array_equal(got[k], ref[k]), k
+    assert sum(len(r) for r in ref) > 0
+
+
 @pytest.mark.parametrize("seg", [1, 3, 7])
 def test_segment_heights_and_patchwork(ws, cascade, seg):
     """Forced short segments (every task boundary, priming and ring wrap-around) and
