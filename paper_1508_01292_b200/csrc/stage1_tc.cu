@@ -13,10 +13,11 @@
 // design minimises the NUMBER of MMAs and the shared-memory A bytes.  Per step:
 //  * layer 1 = implicit GEMM on the tensor core, A in TMEM: TMEM lane m (= P2 column X) holds,
 //    per image row of an 8-row ring, the 8 raw pixels 4X .. 4X+7 (two aligned level words,
-//    exact in fp16); one MMA (M=128, K=16 = two image rows, N=96 = 2 P1 columns (2X, 2X+1) x
-//    2 P1 rows x 4 pool positions x 6 maps) per image-row pair and weight part (w/127.5 * 2^s
+//    exact in fp16); one MMA (M=128, K=16 = two image rows, N=96 = 2 P1 rows x 2 P1 columns
+//    (2X, 2X+1) x 4 pool positions x 6 maps) per image-row pair and weight part (w/127.5 * 2^s
 //    split into fp16 hi + lo, both accumulated in fp32): 8 MMAs produce two P1 rows of the
-//    band's 256 columns, the 2x2 pool cells of every map in one TMEM lane;
+//    band's 256 columns, the 2x2 pool cells of every map in one TMEM lane.  Row pair 0 only
+//    reaches P1 row 0 and row pair 3 only P1 row 1: those MMAs run at N = 48;
 //  * epilogue (4 warps, one TMEM lane each): max over the pool positions, bias, Eq. 1, split
 //    into fp16 hi + lo, stored as 16-B entries (6 channels + 2 zero) in shared-memory planes,
 //    even / odd columns de-interleaved;
@@ -100,6 +101,7 @@ constexpr uint32_t TM_D2 = 128;                // layer-2 accumulators: [half 0 
 constexpr uint32_t TM_D3 = 224;                // layer-3 accumulator (24)
 constexpr uint32_t TM_COLS = 256;
 constexpr uint32_t IDESC = tc05::idesc_f16(128, 96);
+constexpr uint32_t IDESC1_HALF = tc05::idesc_f16(128, 48);  // layer-1 row pairs 0 (P1 row 0), 3 (P1 row 1)
 constexpr uint32_t IDESC2 = tc05::idesc_f16(128, 96);
 constexpr uint32_t IDESC2_LO = tc05::idesc_f16(128, 48);    // lo(A): the w-hi columns only
 constexpr uint32_t IDESC3 = tc05::idesc_f16(128, 24);
@@ -246,21 +248,22 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 tc05::st4(tm + t_lane + TM_A + 4 * (r & 7), h2_of(wv[0], 0x4140), h2_of(wv[0], 0x4342),
                           h2_of(wv[1], 0x4140), h2_of(wv[1], 0x4342));
             };
-            // layer-1 epilogue of unit k: P1 rows 2k, 2k+1 (task-relative), columns 2X + cx -> planes
+            // layer-1 epilogue of unit k: P1 rows 2k + rr (task-relative), columns 2X + cx -> planes;
+            // accumulator column rr * 48 + cx * 24 + pos * 6 + o
             auto l1_epilogue = [&](int k) {
 #pragma unroll 1
-                for (int cx = 0; cx < 2; ++cx) {
+                for (int rr = 0; rr < 2; ++rr) {
                     float d[48];
-                    ld48(tm + t_lane + TM_D1 + 48 * cx, d);
+                    ld48(tm + t_lane + TM_D1 + 48 * rr, d);
 #pragma unroll
-                    for (int rr = 0; rr < 2; ++rr) {
+                    for (int cx = 0; cx < 2; ++cx) {
                         uint32_t hi[3], lo[3];
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
                             float mx[2];
 #pragma unroll
                             for (int e = 0; e < 2; ++e) {
-                                const float* q = d + rr * 24 + 2 * c + e;
+                                const float* q = d + cx * 24 + 2 * c + e;
                                 mx[e] = fmaxf(fmaxf(q[0], q[6]), fmaxf(q[12], q[18]));
                             }
                             const float2 x = __ffma2_rn(make_float2(mx[0], mx[1]), make_float2(W.tcx[14], W.tcx[14]),
@@ -441,17 +444,22 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
             const uint64_t ad2 = tc05::sdesc(s_base + OFF_PL, PL_PAR, 128);
             const uint64_t bd3 = tc05::sdesc(s_base + OFF_B3, 24 * 16, 128);
             const uint64_t ad3 = tc05::sdesc(s_base + OFF_P2, P2_HL, 128);
-            // layer 1 of unit k
+            // layer 1 of unit k: row pair 1 first (N = 96, initialises the accumulator), then
+            // pairs 2 (N = 96), 0 (P1 row 0 only) and 3 (P1 row 1 only) at N = 48
             auto issue_l1 = [&](int k) {
                 if (tc05::elect_one()) {
 #pragma unroll
-                    for (int p = 0; p < 4; ++p)
+                    for (int i = 0; i < 4; ++i) {
+                        const int p = i == 0 ? 1 : i == 1 ? 2 : i == 2 ? 0 : 3;
+                        const uint32_t n0 = p == 3 ? 48u : 0u;          // first accumulator column
 #pragma unroll
                         for (int hl = 0; hl < 2; ++hl) {
                             const uint32_t a = tm + TM_A + 4 * ((4 * k + 2 * p) & 7);
-                            tc05::mma_f16_ts(tm + TM_D1, a, bd1 + (uint64_t)((p * 2 + hl) * (BMAT >> 4)),
-                                             IDESC, (p | hl) != 0);
+                            tc05::mma_f16_ts(tm + TM_D1 + n0, a,
+                                             bd1 + (uint64_t)(((p * 2 + hl) * BMAT + n0 * 16) >> 4),
+                                             (p == 0 || p == 3) ? IDESC1_HALF : IDESC, (i | hl) != 0);
                         }
+                    }
                     tc05::commit(&bar_l1);
                 }
                 __syncwarp();
@@ -554,7 +562,7 @@ int stage1_tc_bmats(const Cnn1W& w, uint16_t* out)
         const float hi = __half2float(__float2half_rn(wp));
         return part ? wp - hi : wp;
     };
-    // layer 1: mat = pair p * 2 + part; n = cx * 48 + rr * 24 + pos * 6 + o (P1 column 2X + cx);
+    // layer 1: mat = pair p * 2 + part; n = rr * 48 + cx * 24 + pos * 6 + o (P1 column 2X + cx);
     // kk = e * 8 + c: image row 2p + e of the unit, pixel 4X + c
     const double sc1 = 1.0 / (double)w.l1_inv_scale;
     for (int p = 0; p < 4; ++p)
@@ -569,7 +577,7 @@ int stage1_tc_bmats(const Cnn1W& w, uint16_t* out)
                                 const int ky = d - 2 * rr - py, kx = c - 2 * cx - px;
                                 if (ky < 0 || ky > 3 || kx < 0 || kx > 3) continue;
                                 const float wp = (float)((double)w.w1[o][ky * 4 + kx] / 127.5 * sc1);
-                                put(out + (p * 2 + part) * (BMAT / 2), 96, cx * 48 + rr * 24 + pos * 6 + o, kk,
+                                put(out + (p * 2 + part) * (BMAT / 2), 96, rr * 48 + cx * 24 + pos * 6 + o, kk,
                                     split(wp, part));
                             }
     // layer 2 (streamed): mat = (par * 2 + rp) * 2 + d, for P1 row 2u + rp of unit u with
