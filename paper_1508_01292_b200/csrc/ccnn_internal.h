@@ -96,6 +96,8 @@ struct LevelInfo {             // one pyramid level of one frame of the batch
 #endif
 constexpr int kPyrCols = 128, kPyrRows = PYR_ROWS, kPyrGroups = 32 / PYR_ROWS;
 constexpr int kPyrTileRows = kPyrRows * kPyrGroups;
+// levels with sigma >= kPyrQuadSigma are resampled 4 columns per thread (pyramid_quad_kernel)
+constexpr double kPyrQuadSigma = 0.7;
 
 // One stage-1 CTA task: a band of TW = 59 window columns x a segment of rows.  Patchwork
 // (SURVEY §8(f) NEXT #1): a band holds up to kMaxPieces pieces of levels
@@ -151,7 +153,7 @@ constexpr int kNmsCap = 4096;  // raw boxes per frame handled by one NMS CTA
 void launch_to_gray(const GrayJob* d_jobs, int n_jobs, int sm_count, cudaStream_t s);
 // use_tex: every frame has a texture object (FrameInfo.tex): 2x2 footprints by tex2Dgather
 void launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, bool safe,
-                    bool use_tex, uint8_t* levels, const LevelInfo* d_levels,
+                    bool any_quad, bool use_tex, uint8_t* levels, const LevelInfo* d_levels,
                     const uint32_t* d_tiles, const uint32_t* d_tabs, cudaStream_t s);
 // stage 1 (fused CNN1 + threshold + compaction): a persistent grid of stage1_grid() CTAs
 // taking tasks[0 .. cta_first[grid]) from an atomic counter, longest first

@@ -66,17 +66,89 @@ __device__ __forceinline__ void load_rows(const uint32_t* __restrict__ yt, uint3
     }
 }
 
-#ifndef PYR_MINB
-#define PYR_MINB 1
-#endif
-template <bool SAFE>
-__global__ void __launch_bounds__(kPyrCols, PYR_MINB) pyramid_kernel(
+// SAFE form for the mildly scaled levels (sigma >= kQuadSigma, e.g. the upscaled levels of
+// small min_face): a thread owns 4 consecutive output columns xo .. xo+3 (one x-table load of
+// 4 entries, one 32-bit store per row) of 8 rows; the CTA's 128 threads cover the same
+// 128 x 32 tile as pyramid_kernel (lane -> column quad, warp -> 8-row group).  The row offset
+// is shared by the 4 columns and 16 byte gathers are in flight before any blend: ~25
+// instructions per pixel instead of ~35, for levels whose 4-column quads stay within a few
+// source sectors per warp (at small sigma the lane stride 4/sigma multiplies the L1
+// wavefronts per gather, and the one-column form wins; K1).
+constexpr double kQuadSigma = kPyrQuadSigma;
+
+__device__ __forceinline__ void quad_tile(const FrameInfo& F, const LevelInfo& L, int tx0, int ty0,
+                                          uint8_t* __restrict__ levels, const uint32_t* __restrict__ tabs)
+{
+    const int pitch = L.pitch;
+    const int xo = tx0 + 4 * (int)(threadIdx.x & 31);
+    const int y_beg = ty0 + 8 * (int)(threadIdx.x >> 5);
+    const int nr = min(8, L.lh - y_beg);
+    if (xo >= pitch || nr <= 0) return;                  // pitch % 16 == 0: xo + 3 < pitch
+    const uint4 xe = __ldg(reinterpret_cast<const uint4*>(tabs + L.tab_off + xo));
+    const uint32_t xs[4] = {xe.x, xe.y, xe.z, xe.w};
+    uint32_t ye[8];
+    {
+        const uint4* yt = reinterpret_cast<const uint4*>(tabs + L.tab_off + pitch + y_beg);
+        const uint4 a = __ldg(yt), b = __ldg(yt + 1);   // padded to kPyrTileRows: no clamp
+        ye[0] = a.x; ye[1] = a.y; ye[2] = a.z; ye[3] = a.w;
+        ye[4] = b.x; ye[5] = b.y; ye[6] = b.z; ye[7] = b.w;
+    }
+    const uint32_t fp = (uint32_t)F.pitch;
+    const uint8_t* __restrict__ src = F.data;
+    uint8_t* dst = levels + L.offset + xo + (int64_t)y_beg * pitch;
+#pragma unroll
+    for (int h = 0; h < 8; h += 2) {
+        int p[2][4][4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const uint32_t row0 = (ye[h + r] & 0xFFFFu) * fp;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t o = row0 + (xs[k] & 0xFFFFu);
+                p[r][k][0] = __ldg(src + o);
+                p[r][k][1] = __ldg(src + o + 1u);
+                p[r][k][2] = __ldg(src + o + fp);
+                p[r][k][3] = __ldg(src + o + fp + 1u);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int ay = (int)(ye[h + r] >> 16);
+            uint32_t w = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                w |= (uint32_t)blend(p[r][k][0], p[r][k][1], p[r][k][2], p[r][k][3], (int)(xs[k] >> 16), ay) << (8 * k);
+            if (h + r < nr) *reinterpret_cast<uint32_t*>(dst + (int64_t)(h + r) * pitch) = w;
+        }
+    }
+}
+
+// the tiles of the levels with sigma >= kQuadSigma (the other tiles exit at once)
+__global__ void __launch_bounds__(kPyrCols) pyramid_quad_kernel(
     const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
     const LevelInfo* __restrict__ lv, const uint32_t* __restrict__ tiles,
     const uint32_t* __restrict__ tabs)
 {
     const FrameInfo F = frames[blockIdx.y];
     if ((int)blockIdx.x >= F.tiles) return;
+    const uint32_t d = __ldg(tiles + F.tile_off + blockIdx.x);
+    const LevelInfo& L = lv[F.level0 + (int)(d & 0xFFu)];
+    if (L.sigma < kQuadSigma) return;
+    quad_tile(F, L, (int)((d >> 8) & 0xFFu) * kPyrCols, (int)(d >> 16) * kPyrTileRows, levels, tabs);
+}
+
+template <bool SAFE>
+__global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
+    const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
+    const LevelInfo* __restrict__ lv, const uint32_t* __restrict__ tiles,
+    const uint32_t* __restrict__ tabs)
+{
+    const FrameInfo F = frames[blockIdx.y];
+    if ((int)blockIdx.x >= F.tiles) return;
+    if (SAFE) {                                                  // CTA-uniform: quad tiles
+        const uint32_t d = __ldg(tiles + F.tile_off + blockIdx.x);   // go to pyramid_quad_kernel
+        if (lv[F.level0 + (int)(d & 0xFFu)].sigma >= kQuadSigma) return;
+    }
     PyrTile T;
     if (!pyr_tile(F, lv, tiles, T)) return;
     const LevelInfo& L = *T.L;
@@ -171,15 +243,18 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_tex_kernel(
 }  // namespace
 
 void launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, bool safe,
-                    bool use_tex, uint8_t* levels, const LevelInfo* d_levels,
+                    bool any_quad, bool use_tex, uint8_t* levels, const LevelInfo* d_levels,
                     const uint32_t* d_tiles, const uint32_t* d_tabs, cudaStream_t s)
 {
     if (n_frames <= 0 || max_tiles <= 0) return;
     const dim3 grid(max_tiles, n_frames);      // frames of other sizes: surplus CTAs exit
     if (use_tex)
         pyramid_tex_kernel<<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
-    else if (safe)
+    else if (safe) {
         pyramid_kernel<true><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
+        if (any_quad)
+            pyramid_quad_kernel<<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
+    }
     else
         pyramid_kernel<false><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
 }

@@ -92,6 +92,7 @@ struct ccnn_ctx {
     int64_t windows_total = 0;
     int pyr_tiles = 0;                  // largest per-frame pyramid tile count
     bool all_safe = true;               // every frame W, H >= 2 (pyramid fast path)
+    bool any_quad = false;              // some level has sigma >= kPyrQuadSigma
     std::vector<int32_t> frame_level0, frame_nlevels, frame_tiles, frame_tile_off;
     std::vector<uint32_t> ptiles;       // pyramid tile descriptors (pyramid.cu)
 
@@ -115,7 +116,7 @@ struct ccnn_ctx {
         int n = 0, n_jobs = 0;
         uint32_t cand_cap = 0;
         int64_t windows = 0;
-        bool timed = false, empty = false;
+        bool timed = false, empty = false, quad = false;
     } slot[2];
     cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
     cudaStream_t pyr_stream = nullptr;  // pyramids (overlap the previous batch's stage 1..NMS)
@@ -375,6 +376,7 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
     c->ptiles.clear();
     c->pyr_tiles = 0;
     c->all_safe = true;
+    c->any_quad = false;
     const double sf = (double)key.scale_step;
     int64_t off = 0, map_off = 0;
     c->windows_total = 0;
@@ -403,6 +405,7 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
             L.nx = (lw - kWinW) / kStep + 1;
             L.ny = (lh - kWinH) / kStep + 1;
             L.frame = f;
+            c->any_quad = c->any_quad || s >= kPyrQuadSigma;
             if (have_tabs) {
                 L.tab_off = it->second[k];
             } else {
@@ -725,6 +728,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     sl.n = n;
     sl.windows = ctx->windows_total;
     sl.timed = timed != 0;
+    sl.quad = ctx->all_safe && ctx->any_quad && !(ctx->debug & CCNN_DEBUG_PYR_TEX);
     sl.empty = (L == 0);                           // empty pyramid: not an error
     ctx->last_W = frames[0].w;
     ctx->last_H = frames[0].h;
@@ -883,7 +887,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     CU(cudaMemcpyAsync(sl.finfo.p, fi, sizeof(FrameInfo) * n, cudaMemcpyHostToDevice, ps));
     const FrameInfo* dfi = sl.finfo.as<FrameInfo>();
     CU(cudaEventRecord(sl.ev[2], ps));
-    launch_pyramid(dfi, n, ctx->pyr_tiles, ctx->all_safe, use_tex, sl.arena.as<uint8_t>(),
+    launch_pyramid(dfi, n, ctx->pyr_tiles, ctx->all_safe, ctx->any_quad, use_tex, sl.arena.as<uint8_t>(),
                    ctx->d_levels.as<LevelInfo>(), ctx->d_ptiles.as<uint32_t>(),
                    ctx->d_tabs.as<uint32_t>(), ps);
     CU(cudaEventRecord(sl.ev[3], ps));
@@ -966,7 +970,7 @@ int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_box
         stats->stage2 = hc.n_stage2;
         stats->stage3 = hc.n_stage3;
         stats->nms = hc.n_out;
-        stats->kernel_launches = 4 + (sl.n_jobs ? 1 : 0);
+        stats->kernel_launches = 4 + (sl.n_jobs ? 1 : 0) + (sl.quad ? 1 : 0);
         const int from[5] = {0, 2, 7, 4, 5}, to[5] = {1, 3, 4, 5, 6};
         for (int k = 0; k < 5; ++k) {
             float t = 0.f;

@@ -521,12 +521,16 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     if (mma_warp) tc05::tmem_dealloc(tm, TM_COLS);
 }
 
+// shared-memory carveout: 2 CTAs x 93 KB fit the 196 KB configuration (86% of 228 KB); the rest
+// of the unified L1 stays cache for the level loads and the overlapped pyramid (K1)
+constexpr int kCarveoutPct = 86;
+
 template <bool DEBUG>
 int occupancy()
 {
     cudaFuncSetAttribute(stage1_tc_kernel<DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(stage1_tc_kernel<DEBUG>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
+                         kCarveoutPct);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stage1_tc_kernel<DEBUG>, NT, SMEM_BYTES);
     if (const char* v = std::getenv("CCNN_VERBOSE"))
@@ -628,13 +632,13 @@ void launch_stage1_tc(const Cnn1W& w, float T1, const uint16_t* d_bmats, const u
     if (dbg_map) {
         cudaFuncSetAttribute(stage1_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         cudaFuncSetAttribute(stage1_tc_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             (int)cudaSharedmemCarveoutMaxShared);
+                             kCarveoutPct);
         stage1_tc_kernel<true><<<grid, NT, SMEM_BYTES, s>>>(w, T1, d_bmats, levels, d_levels, d_tasks, d_cta_first,
                                                             cands, cand_cap, ctrl, dbg_map);
     } else {
         cudaFuncSetAttribute(stage1_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         cudaFuncSetAttribute(stage1_tc_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             (int)cudaSharedmemCarveoutMaxShared);
+                             kCarveoutPct);
         stage1_tc_kernel<false><<<grid, NT, SMEM_BYTES, s>>>(w, T1, d_bmats, levels, d_levels, d_tasks, d_cta_first,
                                                              cands, cand_cap, ctrl, nullptr);
     }
