@@ -363,8 +363,8 @@ def main():
                          "peak_note": "dense fp16/bf16 tensor peak, measured sustained "
                                       "(MEASURED_PEAKS.json bf16_tflops_sustained); achieved = "
                                       "ALGORITHMIC fp32-equivalent FLOPs of CNN1 / measured stage-1 time. "
-                                      "The MMAs actually issued are ~8x that (hi+lo splits, implicit-GEMM "
-                                      "zero taps; DESIGN.md K2); ncu: tc pipe 88% busy (operand fetch)",
+                                      "The MMAs actually issued are ~6x that (hi+lo splits, implicit-GEMM "
+                                      "zero taps; DESIGN.md K2); ncu: tc pipe ~80% busy",
                          "fp32_ffma_peak": fp32_peak,
                          "frac_of_fp32_ffma_peak": achieved_tflops / fp32_peak},
             "e2e": {"value": world * batch * e2e_steps / (ms_e2e / 1000.0), "unit": "frames/s",

@@ -453,8 +453,10 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
     const int TW = c->s1_tc ? stage1_tc_band_width() : stage1_band_width();
     auto task_cost = [&](int nrows) { return c->s1_tc ? stage1_tc_task_cost(nrows) : stage1_task_cost(nrows); };
     // segment height: the tallest segments (least vertical halo recompute) whose largest
-    // task still fits in half the average load of a CTA slot, so the dynamic list schedule
-    // balances (ccnn_params.segment_rows > 0 forces a height)
+    // task still fits in the average load of a CTA slot, so the dynamic longest-first list
+    // schedule balances (measured at C4 with the tcgen05 kernel: full-height bands 0.418 ms
+    // vs 0.452 at the former half-load rule's 128 rows; ccnn_params.segment_rows > 0 forces
+    // a height)
     // bands: every full TW-wide band of a level is its own band; the tail pieces (the last,
     // narrower band of each level, or a whole narrow level) are packed side by side into
     // shared bands, first-fit by decreasing height (patchwork)
@@ -525,7 +527,7 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
                 total += task_cost(t.nrows);
                 biggest = std::max<int64_t>(biggest, task_cost(t.nrows));
             }
-            if (2 * biggest * c->s1_grid <= total) break;
+            if (biggest * c->s1_grid <= total) break;
         }
     }
     // tasks of all frames in one list, longest first (cost ~ super-steps, independent of the
