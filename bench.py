@@ -5,7 +5,7 @@ Contract:
   N > 1: launched by torchrun, one rank per GPU, frames sharded by rank (weak scaling);
   NCCL is used once, for the final all_gather of the detections.
 A step = one batch of synthetic frames through the public API (ccnn_submit + ccnn_collect,
-two batches in flight; pyramid -> fused stage 1 -> selective unit -> NMS -> boxes on the host).  `value` is timed with CUDA events on the
+three batches in flight; pyramid -> fused stage 1 -> selective unit -> NMS -> boxes on the host).  `value` is timed with CUDA events on the
 ctx stream with the batch already resident in HBM (265 MB of 4K frames per step, larger
 than the 126 MB L2); `e2e` is the same call with the frames in pinned HOST memory
 (H2D inside the timed region).  Rank 0 prints ONE JSON line.
@@ -262,13 +262,15 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s1_ms, launches, all_boxes = 0.0, 0, []
     stats = None
-    # the streaming public API (ccnn_submit / ccnn_collect) with two batches in flight: batch
-    # k+1 is enqueued before batch k's boxes are collected, so the host's per-call work and the
-    # D2H of the boxes overlap the device work (each step still produces its boxes on the host)
+    # the streaming public API (ccnn_submit / ccnn_collect) with three batches in flight: batch
+    # k+2 is enqueued before batch k's boxes are collected, so the host's per-call work, the D2H
+    # of the boxes and the next batches' pyramids overlap the device work (each step still
+    # produces its boxes on the host)
     e0.record(stream)
-    det.submit(dframes, cfg.min_face, cfg.scale_step)
+    for k in range(min(2, args.steps)):
+        det.submit(dframes, cfg.min_face, cfg.scale_step)
     for k in range(args.steps):
-        if k + 1 < args.steps:
+        if k + 2 < args.steps:
             det.submit(dframes, cfg.min_face, cfg.scale_step)
         b = det.collect()
         stats = det.last_stats
@@ -292,7 +294,7 @@ def main():
 
     # ---- e2e: the streaming public API (ccnn_submit / ccnn_collect) with the frames in
     #      pinned HOST memory: every step copies its 265 MB H2D and reads its boxes back;
-    #      the copy of step k+1 overlaps the kernels of step k (two batches in flight) ----
+    #      the copy of step k+1 overlaps the kernels of step k (three batches in flight) ----
     e2e_steps = args.e2e_steps or max(3, args.steps // 2)
     old_aff = bind_host_to_gpu(dev.index)
     host = torch.from_numpy(frames).pin_memory()
@@ -302,11 +304,12 @@ def main():
     h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     h0.record(stream)
     d2h = 0
-    det.submit(host, cfg.min_face, cfg.scale_step, timed=False)
-    for k in range(1, e2e_steps):
+    for k in range(min(2, e2e_steps)):
         det.submit(host, cfg.min_face, cfg.scale_step, timed=False)
+    for k in range(e2e_steps):
+        if k + 2 < e2e_steps:
+            det.submit(host, cfg.min_face, cfg.scale_step, timed=False)
         d2h += det.collect().nbytes + 64
-    d2h += det.collect().nbytes + 64
     h1.record(stream)
     h1.synchronize()
     barrier()

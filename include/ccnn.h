@@ -150,11 +150,14 @@ int ccnn_detect_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
 
 /* Streaming form of ccnn_detect (a video stream).
  * ccnn_submit enqueues one batch (same arguments as ccnn_detect) and returns at once: host
- * frames are copied H2D on an internal copy stream into one of two per-ctx frame buffers,
- * so the copy of batch k+1 overlaps the kernels of batch k; host frames must stay valid
- * (and should be pinned) until the batch is collected; device frames until then too.
- * At most two batches may be in flight (CCNN_E_STATE otherwise); timed != 0 records the
- * per-stage events reported by ccnn_collect's stats.
+ * frames are copied H2D on an internal copy stream into one of three per-ctx frame buffers,
+ * so the copy of batch k+1 overlaps the kernels of batch k; each batch's pyramid runs on a
+ * low-priority internal stream in the background of the earlier batches' stage 1 .. NMS
+ * (high-priority internal stream); both start after an event recorded on the ctx stream at
+ * submit time.  Host frames must stay valid (and should be pinned) until the batch is
+ * collected; device frames until then too.  At most three batches may be in flight
+ * (CCNN_E_STATE otherwise); timed != 0 records the per-stage events reported by
+ * ccnn_collect's stats.
  * ccnn_collect waits for the OLDEST in-flight batch and returns its boxes exactly like
  * ccnn_detect (including CCNN_E_CAPACITY + ccnn_last_boxes).  ccnn_detect = submit +
  * collect and is refused while batches are in flight.  Do not change the stream while

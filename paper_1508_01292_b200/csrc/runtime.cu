@@ -100,7 +100,9 @@ struct ccnn_ctx {
     DevBuf d_levels, d_tasks, d_cta_first, d_tabs, d_ptiles, cands, selout, dbg_resp, acc, staging,
         counts, dbg_map;
 
-    // per in-flight batch (ccnn_submit / ccnn_collect ping-pong, NEXT #2 streaming ingest)
+    // per in-flight batch (ccnn_submit / ccnn_collect, NEXT #2 streaming ingest): three slots,
+    // so the pyramid of batch k+2 can run in the background of batches k and k+1
+    static constexpr int kSlots = 3;
     struct Slot {
         DevBuf frames;              // H2D destination (host input)
         DevBuf finfo;               // FrameInfo[n] of the batch
@@ -117,7 +119,7 @@ struct ccnn_ctx {
         uint32_t cand_cap = 0;
         int64_t windows = 0;
         bool timed = false, empty = false, quad = false;
-    } slot[2];
+    } slot[kSlots];
     cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
     cudaStream_t pyr_stream = nullptr;  // pyramids (overlap the previous batch's stage 1..NMS)
     cudaStream_t comp = nullptr;        // stage 1 .. NMS; ordered after the user's stream
@@ -703,7 +705,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
             return fail(ctx, CCNN_E_ARG, "level 0 too large (min_face too small for this frame)");
         key.dims.emplace_back(F.w, F.h);
     }
-    if (ctx->inflight >= 2) return fail(ctx, CCNN_E_STATE, "two batches in flight: ccnn_collect first");
+    if (ctx->inflight >= ccnn_ctx::kSlots) return fail(ctx, CCNN_E_STATE, "three batches in flight: ccnn_collect first");
     CU(cudaSetDevice(ctx->device));
     // device work: pyramid on pyr_stream, the rest on comp; both start after an event recorded
     // on the user's stream (device frames written there are complete), so batch k+1's pyramid
@@ -739,7 +741,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
         sl.cand_cap = 0;
         sl.n_jobs = 0;
         CU(cudaEventRecord(sl.ev[6], s));
-        ctx->next_slot ^= 1;
+        ctx->next_slot = (ctx->next_slot + 1) % ccnn_ctx::kSlots;
         ctx->inflight++;
         return CCNN_OK;
     }
@@ -827,7 +829,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
         }
         cudaStream_t cs = frames_on_device ? ctx->stream : ctx->copy_stream;
         if (!frames_on_device) {
-            // the previous batch of this slot (k-2) read these buffers until its end event
+            // the previous batch of this slot (k - kSlots) read these buffers until its end event
             if (sl.used) CU(cudaStreamWaitEvent(ctx->copy_stream, sl.ev[6], 0));
         }
         CU(cudaEventRecord(sl.ev[0], cs));
@@ -919,7 +921,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     CU(cudaMemcpyAsync(sl.h_ctrl, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
     CU(cudaEventRecord(sl.ev[6], s));
     sl.used = true;
-    ctx->next_slot ^= 1;
+    ctx->next_slot = (ctx->next_slot + 1) % ccnn_ctx::kSlots;
     ctx->inflight++;
     return CCNN_OK;
 }
@@ -941,7 +943,7 @@ int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_box
     if (!n_boxes || (box_cap > 0 && !boxes)) return fail(ctx, CCNN_E_ARG, "NULL n_boxes / boxes");
     if (ctx->inflight == 0) return fail(ctx, CCNN_E_STATE, "no batch in flight");
     CU(cudaSetDevice(ctx->device));
-    const int si = ctx->next_slot ^ (ctx->inflight == 2 ? 0 : 1);     // oldest in-flight slot
+    const int si = (ctx->next_slot - ctx->inflight + ccnn_ctx::kSlots) % ccnn_ctx::kSlots;   // oldest in-flight slot
     ccnn_ctx::Slot& sl = ctx->slot[si];
     ctx->inflight--;
     ctx->last_slot = si;

@@ -247,18 +247,21 @@ def test_streaming_submit_collect(ws):
         det.detect(batches[0], c.min_face, c.scale_step)
     assert e.value.code == ccnn.CCNN_E_STATE
     det.submit(pinned[0], c.min_face, c.scale_step)
-    with pytest.raises(ccnn.CcnnError) as e:         # a third batch is refused
-        det.submit(pinned[1], c.min_face, c.scale_step)
+    det.submit(pinned[1], c.min_face, c.scale_step)     # three in flight
+    with pytest.raises(ccnn.CcnnError) as e:         # a fourth batch is refused
+        det.submit(pinned[2], c.min_face, c.scale_step)
     assert e.value.code == ccnn.CCNN_E_STATE
+    got.append(det.collect())
     got.append(det.collect())
     got.append(det.collect())
     for k in range(4):
         assert np.array_equal(got[k], ref[k])
     assert np.array_equal(got[4], ref[0])
+    assert np.array_equal(got[5], ref[1])
 
 
 def test_streaming_device_frames_overlapped_pyramid(ws):
-    """The bench's path: device-resident batches, two in flight, so batch k+1's pyramid (own
+    """The bench's path: device-resident batches, three in flight, so batch k+2's pyramid (own
     stream, own level arena) overlaps batch k's stage 1 .. NMS: results equal the synchronous
     ccnn_detect of each batch, in order (C4 4K frames, distinct content per batch)."""
     import torch
@@ -270,9 +273,11 @@ def test_streaming_device_frames_overlapped_pyramid(ws):
     ref = [det.detect(b, c.min_face, c.scale_step) for b in batches]
     got = []
     det.submit(batches[0], c.min_face, c.scale_step)
-    for k in range(1, len(batches)):
+    det.submit(batches[1], c.min_face, c.scale_step)
+    for k in range(2, len(batches)):                  # three in flight
         det.submit(batches[k], c.min_face, c.scale_step)
         got.append(det.collect())
+    got.append(det.collect())
     got.append(det.collect())
     for k in range(len(batches)):
         assert np.array_equal(got[k], ref[k]), k
