@@ -161,6 +161,10 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
     const int pitch = L.pitch;
     uint8_t* dst = levels + L.offset + T.xo + (int64_t)T.y_beg * pitch;
     const uint32_t* yt = tabs + L.tab_off + pitch + T.y_beg;   // padded: no clamp
+    // frames are < 4 GB: 32-bit row offsets from this column's base pointer (SAFE: the
+    // second row is one pitch further, the second column one byte)
+    const uint32_t fp = (uint32_t)F.pitch;
+    const uint8_t* __restrict__ col = F.data + x0;
     for (int g0 = 0; g0 < T.nr; g0 += kPyrRows) {             // CTA-uniform
         const int nr = T.nr - g0;
         uint32_t ye[kPyrRows];
@@ -169,13 +173,22 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
 #pragma unroll
         for (int r = 0; r < kPyrRows; ++r) {
             const uint32_t y0 = ye[r] & 0xFFFFu;
-            const uint32_t y1 = SAFE ? y0 + 1u : min(y0 + 1u, (uint32_t)(F.h - 1));
-            const uint8_t* r0 = F.data + (int64_t)y0 * F.pitch;
-            const uint8_t* r1 = F.data + (int64_t)y1 * F.pitch;
-            p[r][0] = __ldg(r0 + x0);
-            p[r][1] = __ldg(r0 + x1);
-            p[r][2] = __ldg(r1 + x0);
-            p[r][3] = __ldg(r1 + x1);
+            if (SAFE) {
+                const uint8_t* r0 = col + y0 * fp;
+                const uint8_t* r1 = r0 + fp;
+                p[r][0] = __ldg(r0);
+                p[r][1] = __ldg(r0 + 1);
+                p[r][2] = __ldg(r1);
+                p[r][3] = __ldg(r1 + 1);
+            } else {
+                const uint32_t y1 = min(y0 + 1u, (uint32_t)(F.h - 1));
+                const uint8_t* r0 = F.data + (int64_t)y0 * F.pitch;
+                const uint8_t* r1 = F.data + (int64_t)y1 * F.pitch;
+                p[r][0] = __ldg(r0 + x0);
+                p[r][1] = __ldg(r0 + x1);
+                p[r][2] = __ldg(r1 + x0);
+                p[r][3] = __ldg(r1 + x1);
+            }
         }
         uint8_t* d = dst + (int64_t)g0 * pitch;
         if (nr >= kPyrRows) {
