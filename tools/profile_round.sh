@@ -16,4 +16,4 @@ done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:selective -s 2 -c 1 -o gpurun_out/prof_selective_c5_$TAG python bench.py --config c5 --steps 1 --warmup 2 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_selective_c5_$TAG.log 2>&1
 timeout 600 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -k "c1_parity_calibrated or edge_cases or rgb_ingest or mixed_size_frames_api" > gpurun_out/memcheck_$TAG.log 2>&1; echo "memcheck rc=$?" >> gpurun_out/memcheck_$TAG.log
 timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -k "c1_parity_calibrated or segment_heights_and_patchwork and 3" > gpurun_out/racecheck_$TAG.log 2>&1; echo "racecheck rc=$?" >> gpurun_out/racecheck_$TAG.log
-tail -3 gpurun_out/tests_$TAG.log; tail -2 gpurun_out/memcheck_$TAG.log gpurun_out/racecheck_$TAG.log
+tail -3 gpurun_out/tests_$TAG.log; tail -n 2 gpurun_out/memcheck_$TAG.log; tail -n 2 gpurun_out/racecheck_$TAG.log
