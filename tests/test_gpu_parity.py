@@ -69,6 +69,18 @@ def test_ragged_multi_frame_batch(ws, cascade, pyr):
     print(rep)
 
 
+def test_legacy_stage1_kernel(ws, cascade, monkeypatch):
+    """The FFMA / mma.sync stage-1 kernel (stage1.cu, v8, kept as the ablation of the tcgen05
+    form; selected by CCNN_S1_LEGACY=1 at ccnn_create) on the ragged multi-frame batch."""
+    monkeypatch.setenv("CCNN_S1_LEGACY", "1")
+    fr = synth_frames.make_stills(3, 333, 257, 991, 20)
+    T1 = quantile_T1(cascade, fr, 20, 1.1, 0.995)
+    T2 = (0.8, 0.1)
+    det = make_det(ws, T1, T2, 1, 0)
+    rep = parity.compare_run(det, cascade, fr, 20, 1.1, T1, T2, 1, 0)
+    print(rep)
+
+
 def test_fddb_like_stills(ws, cascade):
     """C2 settings (minSize 15, scaleFactor 1.05: 67 levels) on 2 of the 450x450 stills."""
     c = configs.C2
