@@ -122,6 +122,8 @@ struct ccnn_ctx {
     } slot[kSlots];
     cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
     cudaStream_t pyr_stream = nullptr;  // pyramids (overlap the previous batch's stage 1..NMS)
+    cudaEvent_t epoch = nullptr;        // CCNN_TIMELINE=1: per-batch event timestamps at collect
+    int64_t batch_no = 0;
     cudaStream_t comp = nullptr;        // stage 1 .. NMS; ordered after the user's stream
                                         // (ccnn_set_stream) through the frames-ready event
     int next_slot = 0, inflight = 0;
@@ -676,6 +678,7 @@ void ccnn_destroy(ccnn_ctx* ctx)
     if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
     if (ctx->pyr_stream) cudaStreamDestroy(ctx->pyr_stream);
     if (ctx->comp) cudaStreamDestroy(ctx->comp);
+    if (ctx->epoch) cudaEventDestroy(ctx->epoch);
     delete ctx;
 }
 
@@ -891,6 +894,10 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     CU(cudaMemcpyAsync(sl.finfo.p, fi, sizeof(FrameInfo) * n, cudaMemcpyHostToDevice, ps));
     const FrameInfo* dfi = sl.finfo.as<FrameInfo>();
     CU(cudaEventRecord(sl.ev[2], ps));
+    if (ctx->epoch == nullptr && std::getenv("CCNN_TIMELINE")) {
+        CU(cudaEventCreate(&ctx->epoch));
+        CU(cudaEventRecord(ctx->epoch, ps));
+    }
     launch_pyramid(dfi, n, ctx->pyr_tiles, ctx->all_safe, ctx->any_quad, use_tex, sl.arena.as<uint8_t>(),
                    ctx->d_levels.as<LevelInfo>(), ctx->d_ptiles.as<uint32_t>(),
                    ctx->d_tabs.as<uint32_t>(), ps);
@@ -982,6 +989,14 @@ int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_box
             stats->ms[k] = t;
         }
     }
+    if (ctx->epoch && sl.timed) {          // timeline diagnostics (ms since the first pyramid)
+        const int ids[6] = {2, 3, 7, 4, 5, 6};
+        float t[6] = {};
+        for (int k = 0; k < 6; ++k) cudaEventElapsedTime(&t[k], ctx->epoch, sl.ev[ids[k]]);
+        std::fprintf(stderr, "ccnn timeline batch %lld: pyr %.4f-%.4f s1 %.4f-%.4f sel-%.4f end %.4f\n",
+                     (long long)ctx->batch_no, t[0], t[1], t[2], t[3], t[4], t[5]);
+    }
+    ++ctx->batch_no;
     *n_boxes = hc.n_out;
     ctx->last_nout = hc.n_out;
     if ((int64_t)hc.n_out > box_cap)
