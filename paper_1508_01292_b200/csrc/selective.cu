@@ -68,7 +68,10 @@ struct SelSmem {
     float wmax[kSelThreads / 32];
     int cand;
 };
-constexpr size_t kP1Floats = 2 * 8 * 26 * kP1RS;    // pooled layer 1, one chunk of 8 maps: [orient][map][y][row]
+// one P1 map plane: 26 rows + 4 floats of padding, so the planes of maps 2c and 2c+2 (the
+// 4 lane groups of a layer-1 MMA epilogue store) start 8 banks apart: conflict-free stores
+constexpr int kP1MS = 26 * kP1RS + 4;
+constexpr size_t kP1Floats = 2 * 8 * kP1MS;    // pooled layer 1, one chunk of 8 maps: [orient][map][y][row]
 
 // E(x, y) normalised (O3), for the FFMA layer 1 of CNN3
 __device__ __forceinline__ float img_at(const SelSmem& sm, int y, int x)
@@ -152,9 +155,9 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
             mma16816(dB, e0, e1, e2, e3, bl0, bl1);
             const float m0 = fmaxf(fmaxf(dA[0], dA[2]), fmaxf(dB[0], dB[2]));
             const float m1 = fmaxf(fmaxf(dA[1], dA[3]), fmaxf(dB[1], dB[3]));
-            float* const dst = p1 + ((o * AC + 2 * c4) * 26 + py) * kP1RS + col;
+            float* const dst = p1 + (o * AC + 2 * c4) * kP1MS + py * kP1RS + col;
             dst[0] = act(fmaf(m0, W.l1_inv_scale, bias0));
-            dst[26 * kP1RS] = act(fmaf(m1, W.l1_inv_scale, bias1));
+            dst[kP1MS] = act(fmaf(m1, W.l1_inv_scale, bias1));
         }
     } else {
     // ---- layer 1: conv4x4 1->A, pool, act; item = (orientation, pooled pos), all A maps ----
@@ -188,7 +191,7 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
                         sv[p] = fmaf(W.w1[a][ky * 4 + kx], x[(p >> 1) + ky][(p & 1) + kx], sv[p]);
             }
             const int col = (px0 & 1) ? kP1Odd + (px0 >> 1) : (px0 >> 1);
-            p1[((o * AC + a) * 26 + py0) * kP1RS + col] =
+            p1[(o * AC + a) * kP1MS + py0 * kP1RS + col] =
                 act(fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3])));   // pool then act
         }
     }
@@ -199,7 +202,7 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
     if (l2_item) {
 #pragma unroll 1
         for (int a = 0; a < AC; ++a) {              // uniform counter: LDCU [UR+imm]
-            const float* in = p1 + ((o2 * AC + a) * 26 + 2 * py2) * kP1RS;
+            const float* in = p1 + (o2 * AC + a) * kP1MS + 2 * py2 * kP1RS;
             float v[4][4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
