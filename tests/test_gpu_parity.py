@@ -155,6 +155,89 @@ def test_c4_full_size_bench_config(ws, cascade):
             assert gb == obx
 
 
+def _sampled_full_size(ws, cascade, c, n_cands, n_windows, full_frames, queue_capacity=4096):
+    """BASELINE config c at full size in the bench's batch and launch configuration
+    (production kernels, no debug map): a sample of the survivors through the per-window
+    oracle and the oracle's selective unit (score within 1e-4; K2, K3, delta exact unless a
+    response lies within 1e-4 of T2; raw box exact), sampled windows one by one vs the
+    survivor set, and the full oracle detection of some frames vs their boxes."""
+    T1, T2 = c.thresholds()
+    fr = c.make_frames()
+    det = make_det(ws, T1, T2, c.Tnn, c.rule, max_w=c.width, max_h=c.height, max_batch=len(fr),
+                   queue_capacity=queue_capacity)
+    boxes = det.detect(fr, c.min_face, c.scale_step)
+    cands = det.candidates()
+    assert det.last_stats["stage1"] == len(cands) > 0
+    lv = oracle.level_table(c.width, c.height, c.min_face, c.scale_step)
+    params = oracle.make_params(T1, T2, c.Tnn, c.rule)
+    rng = np.random.default_rng(11)
+    lev_cache = {}
+
+    def level(f, l):
+        if (f, l) not in lev_cache:
+            s, w, h = lv[l]
+            lev_cache[(f, l)] = oracle.resample(fr[f], s, w, h)
+        return lev_cache[(f, l)]
+    checked_sel = 0
+    for idx in rng.choice(len(cands), min(n_cands, len(cands)), replace=False):
+        x = cands[idx]
+        f, l, i, j = parity.key(x)
+        s1 = oracle.stage1_window(cascade.nets[0], level(f, l), i, j)
+        assert abs(float(x["s1"]) - s1) <= parity.TOL and s1 > T1 - parity.TOL
+        assert (int(x["bx"]), int(x["by"]), int(x["bw"]), int(x["bh"])) == oracle.raw_box(lv[l][0], i, j)
+        oc = oracle.classify(cascade.nets[1], cascade.nets[2], oracle.extract_patch(fr[f], lv[l][0], i, j), params)
+        near = any(abs(v - T2[0]) <= parity.TOL for v in oc.r2) or \
+            (oc.cnn3_ran and any(abs(v - T2[1]) <= parity.TOL for v in oc.r3))
+        if near:
+            continue
+        assert (int(x["K2"]), int(x["K3"]), int(x["delta"]), int(x["cnn3_ran"])) == \
+            (oc.K2, oc.K3, oc.delta, oc.cnn3_ran)
+        assert abs(float(x["score"]) - oc.score) <= parity.TOL
+        checked_sel += 1
+    assert checked_sel >= 0.9 * min(n_cands, len(cands))
+    gset = {parity.key(x) for x in cands}
+    n_checked = 0
+    for _ in range(n_windows):
+        f = int(rng.integers(len(fr)))
+        l = int(rng.integers(len(lv)))
+        nx, ny = oracle.window_grid(lv[l][1], lv[l][2])
+        i, j = int(rng.integers(ny)), int(rng.integers(nx))
+        s1 = oracle.stage1_window(cascade.nets[0], level(f, l), i, j)
+        if abs(s1 - T1) <= parity.TOL:
+            continue
+        assert ((f, l, i, j) in gset) == (np.float32(s1) > np.float32(T1))
+        n_checked += 1
+    assert n_checked > 0.95 * n_windows
+    for f in full_frames:
+        oc, ob, _ = oracle.detect(cascade, fr[f:f + 1], c.min_face, c.scale_step, T1, T2, c.Tnn, c.rule)
+        oset = {(f, int(k["level"]), int(k["iy"]), int(k["ix"])) for k in oc}
+        diff = oset ^ {k for k in gset if k[0] == f}
+        for (_, l, i, j) in diff:
+            assert abs(oracle.stage1_window(cascade.nets[0], level(f, l), i, j) - T1) <= parity.TOL
+        if not diff and not any(np.any(np.abs(k["r2"] - T2[0]) <= parity.TOL) or
+                                np.any(np.abs(k["r3"] - T2[1]) <= parity.TOL) for k in oc):
+            gb = sorted((int(b["x"]), int(b["y"]), int(b["w"]), int(b["h"]), int(b["neighbors"]))
+                        for b in boxes[boxes["frame"] == f])
+            obx = sorted((int(b["x"]), int(b["y"]), int(b["w"]), int(b["h"]), int(b["neighbors"]))
+                         for b in ob)
+            assert gb == obx
+    return len(cands), checked_sel
+
+
+def test_c5_full_size_clutter_sampled(ws, cascade):
+    """C5: 16 cluttered 4K frames at ~1% stage-1 survival (~50k survivors, the selective-unit
+    and NMS stress), queue capacity as in bench.py."""
+    n, k = _sampled_full_size(ws, cascade, configs.C5, 300, 2000, [0], queue_capacity=40000)
+    assert n > 10000
+    print(n, k)
+
+
+def test_c2_full_size_fddb_sampled(ws, cascade):
+    """C2: 256 FDDB-like 450x450 stills, min face 15 (upscaled levels), scale 1.05."""
+    n, k = _sampled_full_size(ws, cascade, configs.C2, 300, 3000, [0, 255])
+    print(n, k)
+
+
 def test_c4_debug_map_sampled(ws, cascade):
     """Dense stage-1 map of a 4K frame (debug instantiation) at 4000 sampled windows."""
     c = configs.C4
