@@ -238,6 +238,12 @@ def test_c2_full_size_fddb_sampled(ws, cascade):
     print(n, k)
 
 
+def test_c3_full_size_1080p_sampled(ws, cascade):
+    """C3: a batch of 1080p video frames, min face 40, scale 1.2."""
+    n, k = _sampled_full_size(ws, cascade, configs.C3, 300, 3000, [0])
+    print(n, k)
+
+
 def test_c4_debug_map_sampled(ws, cascade):
     """Dense stage-1 map of a 4K frame (debug instantiation) at 4000 sampled windows."""
     c = configs.C4
