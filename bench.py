@@ -54,7 +54,8 @@ def level_table(W, H, min_face, sf):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled (every 20 ms) while the GPU is under load:
+    only the samples taken between mark_load() and stop() are reported (all, if none)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -64,23 +65,28 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.t_load = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
             self.proc = None
 
+    def mark_load(self):
+        self.t_load = time.perf_counter()
+
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
 
     def stop(self):
+        t_end = time.perf_counter()
         if self.proc:
             self.proc.terminate()
             try:
@@ -89,14 +95,17 @@ class ClockSampler:
                 self.proc.kill()
         if not self.rows:
             return None
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        rows = [r for t, r in self.rows if self.t_load is not None and self.t_load <= t <= t_end]
+        window = "load" if rows else "all"
+        rows = rows or [r for _, r in self.rows]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4)
+        reasons = sorted({names[k] for r in rows for k in range(4)
                           if len(r) > 4 + k and r[4 + k].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(rows), "window": window}
 
 
 def parse_cpulist(text):
@@ -259,6 +268,8 @@ def main():
         clocks.start()
         time.sleep(0.3)
     barrier()
+    if clocks:
+        clocks.mark_load()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s1_ms, launches, all_boxes = 0.0, 0, []
     stats = None
@@ -290,7 +301,6 @@ def main():
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    clk = clocks.stop() if clocks else None
 
     # ---- e2e: the streaming public API (ccnn_submit / ccnn_collect) with the frames in
     #      pinned HOST memory: every step copies its 265 MB H2D and reads its boxes back;
@@ -314,6 +324,7 @@ def main():
     h1.synchronize()
     barrier()
     ms_e2e = max(h0.elapsed_time(h1), 1000.0 * (time.perf_counter() - t_e2e0) - 1.0)
+    clk = clocks.stop() if clocks else None     # device-timed + e2e regions (both under load)
     numa = None
     if old_aff is not None:
         numa = f"host pinned to the GPU's NUMA node ({len(os.sched_getaffinity(0))} CPUs)"
