@@ -97,8 +97,7 @@ struct ccnn_ctx {
     std::vector<uint32_t> ptiles;       // pyramid tile descriptors (pyramid.cu)
 
     // shared by consecutive batches (their kernels are ordered on the compute stream)
-    DevBuf d_levels, d_tasks, d_cta_first, d_tabs, d_ptiles, cands, selout, dbg_resp, acc, staging,
-        counts, dbg_map;
+    DevBuf d_levels, d_tasks, d_cta_first, d_tabs, d_ptiles, dbg_resp, dbg_map;
 
     // per in-flight batch (ccnn_submit / ccnn_collect, NEXT #2 streaming ingest): three slots,
     // so the pyramid of batch k+2 can run in the background of batches k and k+1
@@ -112,8 +111,12 @@ struct ccnn_ctx {
         DevBuf ctrl, out;           // control block, compacted boxes
         DevBuf arena;               // all levels of the batch (the pyramid of batch k+1 runs on
                                     // the pyramid stream while batch k's stage 1 reads its own)
+        DevBuf cands, selout, acc, staging, counts;   // survivor queue .. NMS scratch: the
+                                    // selective unit / NMS of batch k (tail stream) overlap
+                                    // the stage 1 of batch k+1 (compute stream)
         Ctrl* h_ctrl = nullptr;     // pinned readback of ctrl
-        cudaEvent_t ev[8] = {};     // h2d0, h2d1, c0, pyramid, stage1, selective, end, stage-1 start
+        cudaEvent_t ev[9] = {};     // h2d0, h2d1, c0, pyramid, stage1, selective, end, stage-1 start,
+                                    // selective start
         bool used = false;          // a batch has been enqueued on this slot before
         int n = 0, n_jobs = 0;
         uint32_t cand_cap = 0;
@@ -124,7 +127,8 @@ struct ccnn_ctx {
     cudaStream_t pyr_stream = nullptr;  // pyramids (overlap the previous batch's stage 1..NMS)
     cudaEvent_t epoch = nullptr;        // CCNN_TIMELINE=1: per-batch event timestamps at collect
     int64_t batch_no = 0;
-    cudaStream_t comp = nullptr;        // stage 1 .. NMS; ordered after the user's stream
+    cudaStream_t tail = nullptr;        // selective unit + NMS + readback of each batch
+    cudaStream_t comp = nullptr;        // stage 1; ordered after the user's stream
                                         // (ccnn_set_stream) through the frames-ready event
     int next_slot = 0, inflight = 0;
 
@@ -632,6 +636,7 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
         CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         CU(cudaStreamCreateWithPriority(&ctx->pyr_stream, cudaStreamNonBlocking, least));
         CU(cudaStreamCreateWithPriority(&ctx->comp, cudaStreamNonBlocking, greatest));
+        CU(cudaStreamCreateWithPriority(&ctx->tail, cudaStreamNonBlocking, greatest));
     }
     *out = ctx;
     return CCNN_OK;
@@ -658,7 +663,7 @@ void ccnn_destroy(ccnn_ctx* ctx)
     cudaDeviceSynchronize();
     drop_textures(ctx, nullptr, 0);
     for (DevBuf* b : {&ctx->d_levels, &ctx->d_tasks, &ctx->d_cta_first, &ctx->d_tabs, &ctx->d_ptiles,
-                      &ctx->cands, &ctx->selout, &ctx->dbg_resp, &ctx->acc, &ctx->staging, &ctx->counts,
+                      &ctx->dbg_resp,
                       &ctx->dbg_map, &ctx->s1_bmats})
         b->release();
     for (auto& sl : ctx->slot) {
@@ -671,6 +676,7 @@ void ccnn_destroy(ccnn_ctx* ctx)
         sl.ctrl.release();
         sl.out.release();
         sl.arena.release();
+        for (DevBuf* b : {&sl.cands, &sl.selout, &sl.acc, &sl.staging, &sl.counts}) b->release();
         if (sl.h_ctrl) cudaFreeHost(sl.h_ctrl);
         for (auto& e : sl.ev) if (e) cudaEventDestroy(e);
     }
@@ -678,6 +684,7 @@ void ccnn_destroy(ccnn_ctx* ctx)
     if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
     if (ctx->pyr_stream) cudaStreamDestroy(ctx->pyr_stream);
     if (ctx->comp) cudaStreamDestroy(ctx->comp);
+    if (ctx->tail) cudaStreamDestroy(ctx->tail);
     if (ctx->epoch) cudaEventDestroy(ctx->epoch);
     delete ctx;
 }
@@ -719,6 +726,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     if (replan) {
         CU(cudaStreamSynchronize(s));              // tables of an in-flight batch stay valid
         CU(cudaStreamSynchronize(ctx->pyr_stream));
+        CU(cudaStreamSynchronize(ctx->tail));
         build_plan(ctx, key);
     }
     const int L = (int)ctx->levels.size();
@@ -757,11 +765,11 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     CU(ctx->d_cta_first.ensure(sizeof(int32_t) * ctx->cta_first.size()));
     CU(ctx->d_tabs.ensure(sizeof(uint32_t) * ctx->tabs.size()));
     CU(ctx->d_ptiles.ensure(sizeof(uint32_t) * std::max<size_t>(1, ctx->ptiles.size())));
-    CU(ctx->cands.ensure(sizeof(S1Cand) * cand_cap));
-    CU(ctx->selout.ensure(sizeof(SelOut) * cand_cap));
-    CU(ctx->acc.ensure(sizeof(AccBox) * cand_cap));
-    CU(ctx->staging.ensure(sizeof(OutBox) * 2 * kNmsCap * (size_t)n));
-    CU(ctx->counts.ensure(sizeof(int32_t) * n));
+    CU(sl.cands.ensure(sizeof(S1Cand) * cand_cap));
+    CU(sl.selout.ensure(sizeof(SelOut) * cand_cap));
+    CU(sl.acc.ensure(sizeof(AccBox) * cand_cap));
+    CU(sl.staging.ensure(sizeof(OutBox) * 2 * kNmsCap * (size_t)n));
+    CU(sl.counts.ensure(sizeof(int32_t) * n));
     CU(sl.out.ensure(sizeof(OutBox) * cand_cap));
     CU(sl.finfo.ensure(sizeof(FrameInfo) * n));
     const bool dbg1 = (ctx->debug & CCNN_DEBUG_STAGE1) != 0;
@@ -872,6 +880,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     if (ctx->tex_cache.size() > 4096) {                // bounded cache: rebuild
         CU(cudaStreamSynchronize(s));
         CU(cudaStreamSynchronize(ctx->pyr_stream));
+        CU(cudaStreamSynchronize(ctx->tail));
         drop_textures(ctx, nullptr, 0);
     }
     // texture-gather pyramid only on request: measured slower than byte gathers on B200
@@ -902,31 +911,38 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
                    ctx->d_levels.as<LevelInfo>(), ctx->d_ptiles.as<uint32_t>(),
                    ctx->d_tabs.as<uint32_t>(), ps);
     CU(cudaEventRecord(sl.ev[3], ps));
+    // stage 1 on the compute stream once the slot's previous batch has finished with the
+    // slot's queue / scratch (its tail) and this batch's pyramid is done
     Ctrl* dctrl = sl.ctrl.as<Ctrl>();
+    if (sl.used) CU(cudaStreamWaitEvent(s, sl.ev[6], 0));
     CU(cudaMemsetAsync(dctrl, 0, sizeof(Ctrl), s));
     CU(cudaStreamWaitEvent(s, sl.ev[3], 0));
     CU(cudaEventRecord(sl.ev[7], s));
     if (ctx->s1_tc)
         launch_stage1_tc(ctx->w1, ctx->T1, ctx->s1_bmats.as<uint16_t>(), sl.arena.as<uint8_t>(),
                          ctx->d_levels.as<LevelInfo>(), ctx->d_tasks.as<S1Task>(), ctx->d_cta_first.as<int32_t>(),
-                         (int)ctx->cta_first.size() - 1, ctx->cands.as<S1Cand>(), cand_cap, dctrl,
+                         (int)ctx->cta_first.size() - 1, sl.cands.as<S1Cand>(), cand_cap, dctrl,
                          dbg1 ? ctx->dbg_map.as<float>() : nullptr, s);
     else
         launch_stage1(ctx->w1, ctx->T1, sl.arena.as<uint8_t>(), ctx->d_levels.as<LevelInfo>(),
                       ctx->d_tasks.as<S1Task>(), ctx->d_cta_first.as<int32_t>(),
-                      (int)ctx->cta_first.size() - 1, ctx->cands.as<S1Cand>(), cand_cap, dctrl,
+                      (int)ctx->cta_first.size() - 1, sl.cands.as<S1Cand>(), cand_cap, dctrl,
                       dbg1 ? ctx->dbg_map.as<float>() : nullptr, s);
     CU(cudaEventRecord(sl.ev[4], s));
+    // selective unit + NMS + readback on the tail stream: they overlap the next batch's stage 1
+    cudaStream_t ts = ctx->tail;
+    CU(cudaStreamWaitEvent(ts, sl.ev[4], 0));
+    CU(cudaEventRecord(sl.ev[8], ts));
     launch_selective(ctx->w2, ctx->w3, ctx->sp, dfi, ctx->d_levels.as<LevelInfo>(),
-                     ctx->cands.as<S1Cand>(), cand_cap, ctx->selout.as<SelOut>(),
-                     dbg1 ? ctx->dbg_resp.as<float>() : nullptr, ctx->acc.as<AccBox>(), dctrl,
-                     ctx->sm_count, s);
-    CU(cudaEventRecord(sl.ev[5], s));
-    launch_nms(ctx->acc.as<AccBox>(), dctrl, n, ctx->min_cluster, ctx->staging.as<OutBox>(),
-               ctx->counts.as<int32_t>(), sl.out.as<OutBox>(), s);
+                     sl.cands.as<S1Cand>(), cand_cap, sl.selout.as<SelOut>(),
+                     dbg1 ? ctx->dbg_resp.as<float>() : nullptr, sl.acc.as<AccBox>(), dctrl,
+                     ctx->sm_count, ts);
+    CU(cudaEventRecord(sl.ev[5], ts));
+    launch_nms(sl.acc.as<AccBox>(), dctrl, n, ctx->min_cluster, sl.staging.as<OutBox>(),
+               sl.counts.as<int32_t>(), sl.out.as<OutBox>(), ts);
     CU(cudaGetLastError());
-    CU(cudaMemcpyAsync(sl.h_ctrl, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
-    CU(cudaEventRecord(sl.ev[6], s));
+    CU(cudaMemcpyAsync(sl.h_ctrl, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, ts));
+    CU(cudaEventRecord(sl.ev[6], ts));
     sl.used = true;
     ctx->next_slot = (ctx->next_slot + 1) % ccnn_ctx::kSlots;
     ctx->inflight++;
@@ -982,7 +998,7 @@ int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_box
         stats->stage3 = hc.n_stage3;
         stats->nms = hc.n_out;
         stats->kernel_launches = 4 + (sl.n_jobs ? 1 : 0) + (sl.quad ? 1 : 0);
-        const int from[5] = {0, 2, 7, 4, 5}, to[5] = {1, 3, 4, 5, 6};
+        const int from[5] = {0, 2, 7, 8, 5}, to[5] = {1, 3, 4, 5, 6};
         for (int k = 0; k < 5; ++k) {
             float t = 0.f;
             cudaEventElapsedTime(&t, sl.ev[from[k]], sl.ev[to[k]]);
@@ -1125,8 +1141,9 @@ int ccnn_debug_candidates(ccnn_ctx* ctx, ccnn_candidate* out, int64_t cap, int64
     std::vector<S1Cand> c(cnt);
     std::vector<SelOut> so(cnt);
     std::vector<float> resp;
-    CU(cudaMemcpyAsync(c.data(), ctx->cands.p, sizeof(S1Cand) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaMemcpyAsync(so.data(), ctx->selout.p, sizeof(SelOut) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    const ccnn_ctx::Slot& ls = ctx->slot[ctx->last_slot];
+    CU(cudaMemcpyAsync(c.data(), ls.cands.p, sizeof(S1Cand) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(so.data(), ls.selout.p, sizeof(SelOut) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
     const bool have_resp = (ctx->debug & CCNN_DEBUG_STAGE1) && ctx->dbg_resp.p;
     if (have_resp) {
         resp.resize((size_t)cnt * 100);
