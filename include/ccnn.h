@@ -25,7 +25,7 @@
  *   - every int-returning function returns CCNN_OK (0) or a negative CCNN_E_* code and
  *     records a message readable with ccnn_last_error(ctx);
  *   - a ccnn_ctx belongs to one CUDA device and is NOT thread-safe (one ctx per thread /
- *     stream); all device work is ordered on the ctx stream (ccnn_set_stream);
+ *     stream); all device work is ordered after the ctx stream (ccnn_set_stream);
  *   - the ctx copies everything it is given at create time; the caller owns `frames`,
  *     `boxes` and `stats` buffers.
  */
@@ -108,8 +108,12 @@ typedef struct ccnn_ctx ccnn_ctx;   /* opaque; owns all device state of one dete
  * *out is set only on success. */
 int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out);
 
-/* Order all later device work of ctx on `cuda_stream` (a cudaStream_t, e.g.
- * torch.cuda.current_stream().cuda_stream); NULL = the legacy default stream. */
+/* Order all later device work of ctx after `cuda_stream` (a cudaStream_t, e.g.
+ * torch.cuda.current_stream().cuda_stream; NULL = the legacy default stream): every
+ * ccnn_detect / ccnn_submit records an event on this stream (after the work the caller
+ * enqueued there, e.g. writing device frames) and the ctx's internal streams (pyramid,
+ * stage 1, selective unit + NMS) start after it.  Completion is reported to the host by
+ * ccnn_detect / ccnn_collect returning. */
 int ccnn_set_stream(ccnn_ctx* ctx, void* cuda_stream);
 
 /* Detect faces in n frames of w x h uint8 grayscale, row pitch `pitch` bytes,
