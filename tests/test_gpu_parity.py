@@ -238,6 +238,15 @@ def test_c2_full_size_fddb_sampled(ws, cascade):
     print(n, k)
 
 
+def test_c4_full_size_selective_all_survivors(ws, cascade):
+    """C4 (the bench workload): every stage-1 survivor through the oracle's selective unit
+    (K2, K3, delta, score, raw box), plus sampled windows and the full oracle boxes of the
+    first frame."""
+    n, k = _sampled_full_size(ws, cascade, configs.C4, 100000, 2000, [0])
+    assert k >= 0.9 * n
+    print(n, k)
+
+
 def test_c3_full_size_1080p_sampled(ws, cascade):
     """C3: a batch of 1080p video frames, min face 40, scale 1.2."""
     n, k = _sampled_full_size(ws, cascade, configs.C3, 300, 3000, [0])
