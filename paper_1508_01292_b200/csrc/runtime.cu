@@ -204,8 +204,8 @@ void unpack_cnn1(const float* w, Cnn1W& o)
     o.b4 = *p;
     {                                                // tensor-core layer-1 fragments
         double mx = 0.0;
-        for (int o = 0; o < 6; ++o)
-            for (int k = 0; k < 16; ++k) mx = std::max(mx, std::fabs((double)o_w1(o, k, w)) / 127.5);
+        for (int m = 0; m < 6; ++m)
+            for (int k = 0; k < 16; ++k) mx = std::max(mx, std::fabs((double)o_w1(m, k, w)) / 127.5);
         // scale so that max |W'| lies in [8, 16): fp16 hi/lo parts stay normal
         const int e = mx > 0.0 ? (int)std::floor(std::log2(mx)) : 0;
         const double sc = std::ldexp(1.0, 3 - e);
