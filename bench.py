@@ -271,7 +271,7 @@ def main():
     if clocks:
         clocks.mark_load()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s1_ms, launches, all_boxes = 0.0, 0, []
+    s1_ms, launches, all_boxes, mma_flops = 0.0, 0, [], 0.0
     stats = None
     # the streaming public API (ccnn_submit / ccnn_collect) with three batches in flight: batch
     # k+2 is enqueued before batch k's boxes are collected, so the host's per-call work, the D2H
@@ -286,6 +286,7 @@ def main():
         b = det.collect()
         stats = det.last_stats
         s1_ms += stats["ms"][2]
+        mma_flops += stats["s1_mma_flops"]
         launches += stats["kernel_launches"]
         all_boxes.append(b)
     # the only cross-GPU exchange: gather every rank's detections (NCCL), once
@@ -377,10 +378,15 @@ def main():
                          "peak_note": "dense fp16/bf16 tensor peak, measured sustained "
                                       "(MEASURED_PEAKS.json bf16_tflops_sustained); achieved = "
                                       "ALGORITHMIC fp32-equivalent FLOPs of CNN1 / measured stage-1 time. "
-                                      "The MMAs actually issued are ~6x that (hi+lo splits, implicit-GEMM "
-                                      "zero taps; DESIGN.md K2); ncu: tc pipe ~80% busy",
+                                      "The MMAs actually issued (mma_issued_*) are ~6x that (hi+lo splits, "
+                                      "implicit-GEMM zero taps; DESIGN.md K2); ncu: tc pipe ~80% busy",
                          "fp32_ffma_peak": fp32_peak,
-                         "frac_of_fp32_ffma_peak": achieved_tflops / fp32_peak},
+                         "frac_of_fp32_ffma_peak": achieved_tflops / fp32_peak,
+                         # the tensor work the kernel actually issues (all MMAs, zero taps and
+                         # hi/lo splits included) over the same time: how busy the tensor
+                         # cores are, as opposed to how much of it the algorithm needs
+                         "mma_issued_tflops": mma_flops / (s1_ms / 1000.0) / 1e12 if s1_ms > 0 else None,
+                         "mma_issued_frac": mma_flops / (s1_ms / 1000.0) / 1e12 / tc_peak if s1_ms > 0 else None},
             "e2e": {"value": world * batch * e2e_steps / (ms_e2e / 1000.0), "unit": "frames/s",
                     "h2d_bytes_per_step": int(frames.nbytes), "d2h_bytes_per_step": int(d2h // e2e_steps),
                     "host_numa": numa},

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define CCNN_ABI_VERSION 3
+#define CCNN_ABI_VERSION 4
 
 /* status codes */
 #define CCNN_OK          0
@@ -99,6 +99,9 @@ typedef struct {
     float   ms[5];             /* device ms: [0] H2D, [1] pyramid, [2] stage 1,
                                   [3] selective, [4] NMS + output (CUDA events) */
     int64_t kernel_launches;   /* kernels this call launched */
+    double  s1_mma_flops;      /* tensor-core work the stage-1 kernel issued for this call
+                                  (2 x M x N x K of every tcgen05.mma: hi+lo splits and the
+                                  implicit GEMMs' zero taps included); 0 for the legacy kernel */
 } ccnn_stats;
 
 typedef struct ccnn_ctx ccnn_ctx;   /* opaque; owns all device state of one detector */

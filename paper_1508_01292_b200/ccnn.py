@@ -61,7 +61,7 @@ class Frame(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("windows", C.c_int64), ("stage1", C.c_int64), ("stage2", C.c_int64),
                 ("stage3", C.c_int64), ("nms", C.c_int64), ("ms", C.c_float * 5),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("s1_mma_flops", C.c_double)]
 
 
 class Candidate(C.Structure):
@@ -193,7 +193,7 @@ class Detector:
         self._check(rc)
         self.last_stats = dict(windows=st.windows, stage1=st.stage1, stage2=st.stage2,
                                stage3=st.stage3, nms=st.nms, ms=list(st.ms),
-                               kernel_launches=st.kernel_launches)
+                               kernel_launches=st.kernel_launches, s1_mma_flops=st.s1_mma_flops)
         return out[:nb.value].copy()
 
     def detect(self, frames, min_face, scale_step, box_cap=None, stream=None):

@@ -90,6 +90,7 @@ struct ccnn_ctx {
     int64_t arena_bytes = 0;            // all levels of all frames
     int64_t map_total = 0;              // dense stage-1 map floats (debug)
     int64_t windows_total = 0;
+    double s1_mma_flops = 0.0;          // tensor-core FLOPs stage 1 issues for the planned batch
     int pyr_tiles = 0;                  // largest per-frame pyramid tile count
     bool all_safe = true;               // every frame W, H >= 2 (pyramid fast path)
     bool any_quad = false;              // some level has sigma >= kPyrQuadSigma
@@ -121,6 +122,7 @@ struct ccnn_ctx {
         int n = 0, n_jobs = 0;
         uint32_t cand_cap = 0;
         int64_t windows = 0;
+        double s1_mma_flops = 0.0;
         bool timed = false, empty = false, quad = false;
     } slot[kSlots];
     cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
@@ -548,6 +550,9 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
     // cta_first = {0, ..., 0, n_tasks}: grid size + total task count for the launch
     const int G = std::max(1, std::min<int>(c->s1_grid, (int)all.size()));
     c->tasks = all;
+    c->s1_mma_flops = 0.0;
+    if (c->s1_tc)
+        for (const S1Task& t : all) c->s1_mma_flops += stage1_tc_task_mma_flops(t.nrows);
     c->cta_first.assign(G + 1, 0);
     c->cta_first[G] = (int32_t)all.size();
 }
@@ -742,6 +747,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     ccnn_ctx::Slot& sl = ctx->slot[ctx->next_slot];
     sl.n = n;
     sl.windows = ctx->windows_total;
+    sl.s1_mma_flops = ctx->s1_mma_flops;
     sl.timed = timed != 0;
     sl.quad = ctx->all_safe && ctx->any_quad && !(ctx->debug & CCNN_DEBUG_PYR_TEX);
     sl.empty = (L == 0);                           // empty pyramid: not an error
@@ -998,6 +1004,7 @@ int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_box
         stats->stage3 = hc.n_stage3;
         stats->nms = hc.n_out;
         stats->kernel_launches = 4 + (sl.n_jobs ? 1 : 0) + (sl.quad ? 1 : 0);
+        stats->s1_mma_flops = sl.s1_mma_flops;
         const int from[5] = {0, 2, 7, 8, 5}, to[5] = {1, 3, 4, 5, 6};
         for (int k = 0; k < 5; ++k) {
             float t = 0.f;

@@ -551,6 +551,17 @@ int occupancy()
 int stage1_tc_band_width() { return TW; }
 int stage1_tc_grid(int sm_count) { return sm_count * std::min(occupancy<false>(), occupancy<true>()); }
 int stage1_tc_task_cost(int nrows) { return nrows + 5 + 2; }
+// tensor-core FLOPs (2 M N K per MMA) the kernel issues for a task of nrows window rows:
+// NQ + 1 layer-1 units and streamed layer-2 P1-row pairs, NQ layer-3 P2 rows (NQ = nrows + 5)
+double stage1_tc_task_mma_flops(int nrows)
+{
+    constexpr double mk = 2.0 * 128 * 16;                            // 2 M K of one MMA
+    constexpr double l1 = mk * (4 * 96 + 4 * 48);                    // row pairs 1, 2 / 0, 3, hi + lo
+    constexpr double l2 = mk * 2 * 2 * (96 + 48);                    // 2 P1 rows x 2 d x (hi(A), lo(A))
+    constexpr double l3 = mk * 5 * 24;                               // 5 kx
+    const int nq = nrows + 5;
+    return (nq + 1) * (l1 + l2) + nq * l3;
+}
 
 // B matrices of the three tensor-core layers (fp16 bit patterns, the kernel's shared-memory
 // image); returns the fp16 count.  K-major canonical layout of one B (N rows, K = 16):
