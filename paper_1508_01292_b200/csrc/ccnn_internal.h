@@ -45,7 +45,8 @@ struct __align__(16) Cnn1W {   // 797 weights + re-arranged copies for the stage
 template <int A, int B, int C>
 struct __align__(16) SelNetW { // CNN2: <16,6,2>, CNN3: <2,2,25>
     static constexpr int W2V = (B * 9 + 3) / 4 * 4;
-    float w2v[A][W2V];         // layer 2 per input map a: [b*9 + ky*3 + kx], float4 blocks
+    float w2v[A][W2V];         // layer 2 per input map a: [(ky*3 + kx)*B + b] (map pairs adjacent
+                               // for the f32x2 FMAs), float4 blocks
     float w1[A][16], b1[A];
     float w2[B][A][9], b2[B];
     float w3[C][B][56], b3[C]; // [out][in][ky*7+kx], 7 wide x 8 tall

@@ -277,7 +277,7 @@ void unpack_sel(const float* p, SelNetW<A, B, C>& o)
     o.b4 = *p;
     for (int a = 0; a < A; ++a)
         for (int k = 0; k < SelNetW<A, B, C>::W2V; ++k)
-            o.w2v[a][k] = k < B * 9 ? o.w2[k / 9][a][k % 9] : 0.f;
+            o.w2v[a][k] = k < B * 9 ? o.w2[k % B][a][k / B] : 0.f;
     // tensor-core layer-1 fragments (used for A == 16): N = 16 maps as two halves of 8
     double mx = 0.0;
     for (int a = 0; a < A; ++a)

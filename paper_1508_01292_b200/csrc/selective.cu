@@ -119,11 +119,12 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
     constexpr int NCH = A / AC;
     const bool l2_item = tid < 2 * 132;
     const int o2 = tid / 132, pos2 = tid - o2 * 132, py2 = pos2 / 11, px2 = pos2 - py2 * 11;
-    float s2[B][4];
+    static_assert(B % 2 == 0, "layer 2 runs on map pairs");
+    float2 s2[B / 2][4];                           // (map 2 bp, map 2 bp + 1) x pool position
 #pragma unroll
-    for (int b = 0; b < B; ++b)
+    for (int bp = 0; bp < B / 2; ++bp)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) s2[b][k] = W.b2[b];
+        for (int k = 0; k < 4; ++k) s2[bp][k] = make_float2(W.b2[2 * bp], W.b2[2 * bp + 1]);
 #pragma unroll 1
     for (int ch = 0; ch < NCH; ++ch) {
     if constexpr (A == 16) {
@@ -220,15 +221,17 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
                 wv[4 * k4] = t4.x; wv[4 * k4 + 1] = t4.y; wv[4 * k4 + 2] = t4.z; wv[4 * k4 + 3] = t4.w;
             }
 #pragma unroll
-            for (int b = 0; b < B; ++b)
+            for (int bp = 0; bp < B / 2; ++bp)
 #pragma unroll
                 for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
                     for (int kx = 0; kx < 3; ++kx) {
-                        const float w = wv[b * 9 + ky * 3 + kx];
+                        const float2 w = make_float2(wv[(ky * 3 + kx) * B + 2 * bp], wv[(ky * 3 + kx) * B + 2 * bp + 1]);
 #pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            s2[b][k] = fmaf(w, v[(k >> 1) + ky][(k & 1) + kx], s2[b][k]);
+                        for (int k = 0; k < 4; ++k) {
+                            const float x = v[(k >> 1) + ky][(k & 1) + kx];
+                            s2[bp][k] = __ffma2_rn(w, make_float2(x, x), s2[bp][k]);
+                        }
                     }
         }
     }
@@ -236,8 +239,12 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
     }
     if (l2_item) {
 #pragma unroll
-        for (int b = 0; b < B; ++b)
-            sm.p2[o2][b][py2][px2] = act(fmaxf(fmaxf(s2[b][0], s2[b][1]), fmaxf(s2[b][2], s2[b][3])));
+        for (int bp = 0; bp < B / 2; ++bp) {
+            sm.p2[o2][2 * bp][py2][px2] =
+                act(fmaxf(fmaxf(s2[bp][0].x, s2[bp][1].x), fmaxf(s2[bp][2].x, s2[bp][3].x)));
+            sm.p2[o2][2 * bp + 1][py2][px2] =
+                act(fmaxf(fmaxf(s2[bp][0].y, s2[bp][1].y), fmaxf(s2[bp][2].y, s2[bp][3].y)));
+        }
     }
     __syncthreads();
     // ---- layer 3: conv7x8 B->C, act; item = (map, orientation, cell) ----
