@@ -54,58 +54,68 @@ def level_table(W, H, min_face, sf):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled (every 20 ms) while the GPU is under load:
-    only the samples taken between mark_load() and stop() are reported (all, if none)."""
+    """SM clocks / throttle reasons sampled every 20 ms by an in-process NVML thread (cheap
+    calls, no driver-lock contention with the measured work) while
+    the GPU is under load: only the samples between mark_load() and stop() are reported (all,
+    if none)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.rows = []                  # (time, sm_mhz, max_mhz, set of reasons)
         self.t_load = None
+        self.stop_ev = threading.Event()
+        self.thread = None
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+        try:
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID("GPU-" + uuid)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "20"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            nv, h = self._nvml_handle()
+            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+
+            def run():
+                while not self.stop_ev.is_set():
+                    try:
+                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((time.perf_counter(), float(sm), float(mx),
+                                          {n for n, bit in zip(self.NAMES, bits) if r & bit}))
+                    except Exception:
+                        pass
+                    self.stop_ev.wait(0.02)
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
         except Exception:
-            self.proc = None
+            self.thread = None
 
     def mark_load(self):
         self.t_load = time.perf_counter()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
-
     def stop(self):
         t_end = time.perf_counter()
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except Exception:
-                self.proc.kill()
+        self.stop_ev.set()
+        if self.thread:
+            self.thread.join(1.0)
         if not self.rows:
             return None
-        rows = [r for t, r in self.rows if self.t_load is not None and self.t_load <= t <= t_end]
+        rows = [r for r in self.rows if self.t_load is not None and self.t_load <= r[0] <= t_end]
         window = "load" if rows else "all"
-        rows = rows or [r for _, r in self.rows]
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in rows for k in range(4)
-                          if len(r) > 4 + k and r[4 + k].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows), "window": window}
+        rows = rows or self.rows
+        return {"sm_mhz": float(np.median([r[1] for r in rows])), "sm_max_mhz": max(r[2] for r in rows),
+                "reasons": sorted(set().union(*[r[3] for r in rows])), "samples": len(rows),
+                "window": window, "source": "nvml"}
 
 
 def parse_cpulist(text):
@@ -306,7 +316,10 @@ def main():
     # ---- e2e: the streaming public API (ccnn_submit / ccnn_collect) with the frames in
     #      pinned HOST memory: every step copies its 265 MB H2D and reads its boxes back;
     #      the copy of step k+1 overlaps the kernels of step k (three batches in flight) ----
-    e2e_steps = args.e2e_steps or max(10, args.steps)      # 265 MB H2D each: ~5.6 ms per step
+    # enough steps for a >= ~100 ms e2e region (host jitter of a few ms must not dominate a
+    # small config's rate): estimate a step from the device-timed loop + H2D at ~40 GB/s
+    est_ms = ms / args.steps + frames.nbytes / 40e9 * 1e3
+    e2e_steps = args.e2e_steps or int(min(2000, max(10, args.steps, np.ceil(100.0 / max(est_ms, 1e-3)))))
     old_aff = bind_host_to_gpu(dev.index)
     host = torch.from_numpy(frames).pin_memory()
     det.detect(host, cfg.min_face, cfg.scale_step)
