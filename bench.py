@@ -320,6 +320,13 @@ def main():
     # small config's rate): estimate a step from the device-timed loop + H2D at ~40 GB/s
     est_ms = ms / args.steps + frames.nbytes / 40e9 * 1e3
     e2e_steps = args.e2e_steps or int(min(2000, max(10, args.steps, np.ceil(100.0 / max(est_ms, 1e-3)))))
+    # per-stage device times of synchronous calls (no neighbouring batches on the GPU): what
+    # each kernel costs alone, e.g. the pyramid's bandwidth (outside the timed regions)
+    alone = []
+    for _ in range(3):
+        det.detect(dframes, cfg.min_face, cfg.scale_step)
+        alone.append(det.last_stats["ms"])
+    alone = [float(x) for x in np.median(np.array(alone), axis=0)]
     old_aff = bind_host_to_gpu(dev.index)
     host = torch.from_numpy(frames).pin_memory()
     det.detect(host, cfg.min_face, cfg.scale_step)
@@ -384,6 +391,10 @@ def main():
             "pipeline_gwindows_per_s": windows_per_frame * total_frames / (ms / 1000.0) / 1e9,
             "stage_ms_per_step": {k: v for k, v in zip(["h2d", "pyramid", "stage1", "selective", "nms_out"],
                                                         stats["ms"])},
+            "stage_ms_alone": {k: v for k, v in zip(["h2d", "pyramid", "stage1", "selective", "nms_out"], alone)},
+            # pyramid: frame read once + levels written once (algorithmic bytes) / its time alone
+            "pyramid_gbs_alone": (frames.nbytes + batch * sum(((w + 15) // 16 * 16) * h for _, w, h in levels))
+                                 / (alone[1] / 1000.0) / 1e9 if alone[1] > 0 else None,
             "table1_counts_last_step": {k: stats[k] for k in ("windows", "stage1", "stage2", "stage3", "nms")},
             "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tc_peak,
                          "unit": "TFLOP/s", "frac": achieved_tflops / tc_peak, "traffic": traffic,
