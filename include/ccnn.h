@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define CCNN_ABI_VERSION 4
+#define CCNN_ABI_VERSION 5
 
 /* status codes */
 #define CCNN_OK          0
@@ -179,8 +179,9 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
                        int min_face, float scale_step, int timed);
 
 /* Copy the boxes of the last ccnn_detect / ccnn_collect on ctx (also valid after it
- * returned CCNN_E_CAPACITY, so a caller can fetch the result without detecting again;
- * valid until the next-but-one ccnn_submit reuses its output buffer).
+ * returned CCNN_E_CAPACITY, so a caller can fetch the result without detecting again).
+ * Valid until the next ccnn_submit / ccnn_detect on ctx: with two batches still in flight
+ * that submit reuses the collected batch's output buffer.
  * *n_boxes = the number of boxes; CCNN_E_CAPACITY if box_cap < *n_boxes. */
 int ccnn_last_boxes(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_boxes);
 
@@ -229,6 +230,16 @@ int ccnn_debug_counters(ccnn_ctx* ctx, uint32_t* out, int cap);
 /* Copy the survivors of the last detect (unordered), *n = total count; out == NULL only
  * queries the count. */
 int ccnn_debug_candidates(ccnn_ctx* ctx, ccnn_candidate* out, int64_t cap, int64_t* n);
+
+/* Run the on-device grouping / NMS (step 4; reading O9) alone on n caller-given raw
+ * boxes (host array; frame in [0, n_frames), x, y >= 0, w, h >= 1, x + w and y + h <= 32767,
+ * finite score; `neighbors` ignored) of n_frames <= max_batch frames, with the ctx's
+ * nms_min_cluster.  Writes the groups to out[0 .. *n_out) in the ccnn_detect output order
+ * (frame, score desc, y, x, w, h).  CCNN_E_QUEUE if a frame has more than 4096 raw boxes,
+ * CCNN_E_CAPACITY if cap < *n_out, CCNN_E_STATE while batches are in flight.  Synchronous;
+ * uses temporary device buffers. */
+int ccnn_debug_group(ccnn_ctx* ctx, const ccnn_box* raw, int64_t n, int n_frames, ccnn_box* out,
+                     int64_t cap, int64_t* n_out);
 
 #ifdef __cplusplus
 }

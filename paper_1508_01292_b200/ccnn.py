@@ -22,7 +22,7 @@ CCNN_DEBUG_LEVELS, CCNN_DEBUG_STAGE1, CCNN_DEBUG_PYR_TEX = 1, 2, 4
 EXPORTS = ("ccnn_create", "ccnn_set_stream", "ccnn_detect", "ccnn_detect_frames",
            "ccnn_submit", "ccnn_collect", "ccnn_submit_frames", "ccnn_last_boxes", "ccnn_destroy", "ccnn_last_error",
            "ccnn_abi_version", "ccnn_set_debug", "ccnn_debug_levels", "ccnn_debug_level",
-           "ccnn_debug_stage1_map", "ccnn_debug_candidates", "ccnn_debug_counters")
+           "ccnn_debug_stage1_map", "ccnn_debug_candidates", "ccnn_debug_counters", "ccnn_debug_group")
 
 
 class CcnnError(RuntimeError):
@@ -117,6 +117,8 @@ def load():
     L.ccnn_debug_stage1_map.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_float), C.c_int64]
     L.ccnn_debug_candidates.argtypes = [C.c_void_p, _P(Candidate), C.c_int64, _P(C.c_int64)]
     L.ccnn_debug_counters.argtypes = [C.c_void_p, _P(C.c_uint32), C.c_int]
+    L.ccnn_debug_group.argtypes = [C.c_void_p, _P(Box), C.c_int64, C.c_int, _P(Box), C.c_int64,
+                                   _P(C.c_int64)]
     _lib = L
     return L
 
@@ -339,3 +341,15 @@ class Detector:
         self._check(L.ccnn_debug_candidates(self.h, buf, n.value, C.byref(n)))
         assert C.sizeof(Candidate) == CAND_DTYPE.itemsize
         return np.frombuffer(bytes(buf), CAND_DTYPE).copy()
+
+    def group(self, raw, n_frames):
+        """ccnn_debug_group: the device NMS alone on raw boxes (BOX_DTYPE array; `neighbors`
+        ignored) of n_frames frames -> grouped boxes in the ccnn_detect output order."""
+        L = load()
+        raw = np.ascontiguousarray(raw, BOX_DTYPE)
+        cap = max(1, len(raw))
+        out = np.zeros(cap, BOX_DTYPE)
+        n = C.c_int64()
+        self._check(L.ccnn_debug_group(self.h, raw.ctypes.data_as(_P(Box)), len(raw), n_frames,
+                                       out.ctypes.data_as(_P(Box)), cap, C.byref(n)))
+        return out[:n.value].copy()

@@ -118,6 +118,7 @@ struct ccnn_ctx {
         Ctrl* h_ctrl = nullptr;     // pinned readback of ctrl
         cudaEvent_t ev[9] = {};     // h2d0, h2d1, c0, pyramid, stage1, selective, end, stage-1 start,
                                     // selective start
+        cudaEvent_t ev_user = nullptr;  // ctx stream at submit (orders the H2D of host frames)
         bool used = false;          // a batch has been enqueued on this slot before
         int n = 0, n_jobs = 0;
         uint32_t cand_cap = 0;
@@ -627,6 +628,7 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
         CU(cudaMallocHost(&sl.h_finfo, sizeof(FrameInfo) * (size_t)p->max_batch));
         CU(cudaMallocHost(&sl.h_jobs, sizeof(GrayJob) * (size_t)p->max_batch));
         for (auto& e : sl.ev) CU(cudaEventCreate(&e));
+        CU(cudaEventCreateWithFlags(&sl.ev_user, cudaEventDisableTiming));
         CU(sl.ctrl.ensure(sizeof(Ctrl)));
     }
     CU(cudaDeviceGetAttribute(&ctx->tex_align, cudaDevAttrTextureAlignment, cuda_device));
@@ -684,6 +686,7 @@ void ccnn_destroy(ccnn_ctx* ctx)
         for (DevBuf* b : {&sl.cands, &sl.selout, &sl.acc, &sl.staging, &sl.counts}) b->release();
         if (sl.h_ctrl) cudaFreeHost(sl.h_ctrl);
         for (auto& e : sl.ev) if (e) cudaEventDestroy(e);
+        if (sl.ev_user) cudaEventDestroy(sl.ev_user);
     }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
@@ -732,6 +735,10 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
         CU(cudaStreamSynchronize(s));              // tables of an in-flight batch stay valid
         CU(cudaStreamSynchronize(ctx->pyr_stream));
         CU(cudaStreamSynchronize(ctx->tail));
+        // the host plan changes now; the device tables only after the uploads below: until
+        // ctx->key = key commits both, a failure (any CU() below) leaves the key invalid so
+        // the next submit replans and re-uploads instead of pairing old tables with a new plan
+        ctx->key = PlanKey{};
         build_plan(ctx, key);
     }
     const int L = (int)ctx->levels.size();
@@ -846,6 +853,10 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
         }
         cudaStream_t cs = frames_on_device ? ctx->stream : ctx->copy_stream;
         if (!frames_on_device) {
+            // the H2D starts after the work the caller enqueued on the ctx stream so far (e.g. a
+            // D2H that fills these pinned host frames), as ccnn_set_stream promises
+            CU(cudaEventRecord(sl.ev_user, ctx->stream));
+            CU(cudaStreamWaitEvent(ctx->copy_stream, sl.ev_user, 0));
             // the previous batch of this slot (k - kSlots) read these buffers until its end event
             if (sl.used) CU(cudaStreamWaitEvent(ctx->copy_stream, sl.ev[6], 0));
         }
@@ -1179,6 +1190,53 @@ int ccnn_debug_candidates(ccnn_ctx* ctx, ccnn_candidate* out, int64_t cap, int64
             std::memcpy(o.r2, &resp[k * 100], sizeof(o.r2));
             std::memcpy(o.r3, &resp[k * 100 + 50], sizeof(o.r3));
         }
+    }
+    return CCNN_OK;
+}
+
+int ccnn_debug_group(ccnn_ctx* ctx, const ccnn_box* raw, int64_t n, int n_frames, ccnn_box* out,
+                     int64_t cap, int64_t* n_out)
+{
+    if (!ctx) return CCNN_E_ARG;
+    if (!n_out || (n > 0 && !raw) || (cap > 0 && !out) || n < 0 || n > 0x7FFFFFFF)
+        return fail(ctx, CCNN_E_ARG, "bad arguments");
+    if (n_frames < 1 || n_frames > ctx->max_batch) return fail(ctx, CCNN_E_ARG, "n_frames out of [1, max_batch]");
+    if (ctx->inflight) return fail(ctx, CCNN_E_STATE, "ccnn_debug_group with batches in flight");
+    std::vector<AccBox> acc((size_t)std::max<int64_t>(n, 1));
+    for (int64_t k = 0; k < n; ++k) {
+        const ccnn_box& b = raw[k];
+        // the NMS kernel holds coordinates as int16 (frames are at most 16384 px)
+        if (b.frame < 0 || b.frame >= n_frames || b.x < 0 || b.y < 0 || b.w < 1 || b.h < 1 ||
+            (int64_t)b.x + b.w > 32767 || (int64_t)b.y + b.h > 32767 || !std::isfinite(b.score))
+            return fail(ctx, CCNN_E_ARG, "raw box out of range");
+        acc[k] = AccBox{b.frame, b.x, b.y, b.w, b.h, b.score};
+    }
+    CU(cudaSetDevice(ctx->device));
+    DevBuf d_acc, d_ctrl, d_staging, d_counts, d_out;
+    struct Guard {
+        DevBuf* b[5];
+        ~Guard() { for (DevBuf* x : b) x->release(); }
+    } guard{{&d_acc, &d_ctrl, &d_staging, &d_counts, &d_out}};
+    CU(d_acc.ensure(sizeof(AccBox) * acc.size()));
+    CU(d_ctrl.ensure(sizeof(Ctrl)));
+    CU(d_staging.ensure(sizeof(OutBox) * 2 * kNmsCap * (size_t)n_frames));
+    CU(d_counts.ensure(sizeof(int32_t) * n_frames));
+    CU(d_out.ensure(sizeof(OutBox) * acc.size()));
+    Ctrl hc{};
+    hc.n_acc = (uint32_t)n;
+    cudaStream_t s = ctx->comp;
+    CU(cudaMemcpyAsync(d_acc.p, acc.data(), sizeof(AccBox) * n, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(d_ctrl.p, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, s));
+    launch_nms(d_acc.as<AccBox>(), d_ctrl.as<Ctrl>(), n_frames, ctx->min_cluster, d_staging.as<OutBox>(),
+               d_counts.as<int32_t>(), d_out.as<OutBox>(), s);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(&hc, d_ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (hc.nms_overflow) return fail(ctx, CCNN_E_QUEUE, "more than 4096 raw boxes in one frame");
+    *n_out = hc.n_out;
+    if ((int64_t)hc.n_out > cap) return fail(ctx, CCNN_E_CAPACITY, "cap < grouped box count");
+    if (hc.n_out) {
+        CU(cudaMemcpy(out, d_out.p, sizeof(OutBox) * hc.n_out, cudaMemcpyDeviceToHost));
     }
     return CCNN_OK;
 }

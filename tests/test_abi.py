@@ -42,7 +42,7 @@ def test_exports_every_declared_symbol(lib):
     assert declared <= exported, declared - exported
     for name in declared:
         getattr(lib, name)
-    assert lib.ccnn_abi_version() == 4
+    assert lib.ccnn_abi_version() == 5
 
 
 def test_sm100a_code_present():

@@ -33,25 +33,37 @@ def quantile_T1(cascade, frames, min_face, sf, q):
     return float(np.float32(np.quantile(allv, q)))
 
 
+def exact(cascade, fr, min_face, sf, q1, rule=0, Tnn=2):
+    """thresholds placed on these frames with a > 1e-4 margin (tests/parity.py)."""
+    T1, T2, margins = parity.exact_thresholds(cascade, fr, min_face, sf, q1, rule=rule, Tnn=Tnn)
+    assert all(m is None or m > parity.TOL for m in margins), margins
+    return T1, T2
+
+
 def test_c1_parity_calibrated(ws, cascade):
+    """The calibrated (Table-1 rate) thresholds on C1: exemptions are possible here, so every
+    frame is compared against the oracle grouping with exempt decisions taken as the GPU's."""
     c = configs.C1
     T1, T2 = c.thresholds()
     fr = c.make_frames()
     det = make_det(ws, T1, T2, c.Tnn, c.rule)
     rep = parity.compare_run(det, cascade, fr, c.min_face, c.scale_step, T1, T2, c.Tnn, c.rule)
+    assert rep["frames_boxes_checked"] == 1
     print(rep)
 
 
 @pytest.mark.parametrize("rule", [0, 1])
 def test_c1_parity_low_threshold(ws, cascade, rule):
-    """T1 at the 97% quantile so ~400 windows reach the selective unit."""
+    """T1 near the 97% quantile so ~400 windows reach the selective unit; thresholds with a
+    margin, so nothing is exempt: survivors, K2/K3/delta, final boxes and Table-1 counts are
+    all exact."""
     c = configs.C1
     fr = c.make_frames()
-    T1 = quantile_T1(cascade, fr, c.min_face, c.scale_step, 0.97)
-    T2 = (0.9, 0.2)
+    T1, T2 = exact(cascade, fr, c.min_face, c.scale_step, 0.97, rule=rule)
     det = make_det(ws, T1, T2, 2, rule)
-    rep = parity.compare_run(det, cascade, fr, c.min_face, c.scale_step, T1, T2, 2, rule)
-    assert rep["survivors"] > 200
+    rep = parity.compare_run(det, cascade, fr, c.min_face, c.scale_step, T1, T2, 2, rule,
+                             expect_exact=True)
+    assert rep["survivors"] > 200 and rep["boxes"] > 0
     print(rep)
 
 
@@ -61,11 +73,12 @@ def test_ragged_multi_frame_batch(ws, cascade, pyr):
     pyramid forms (texture gathers / byte gathers)."""
     from paper_1508_01292_b200 import ccnn
     fr = synth_frames.make_stills(3, 333, 257, 991, 20)
-    T1 = quantile_T1(cascade, fr, 20, 1.1, 0.995)
-    T2 = (0.8, 0.1)
+    T1, T2 = exact(cascade, fr, 20, 1.1, 0.995, Tnn=1)
     det = make_det(ws, T1, T2, 1, 0)
     rep = parity.compare_run(det, cascade, fr, 20, 1.1, T1, T2, 1, 0,
-                             debug_extra=ccnn.CCNN_DEBUG_PYR_TEX if pyr == "tex" else 0)
+                             debug_extra=ccnn.CCNN_DEBUG_PYR_TEX if pyr == "tex" else 0,
+                             expect_exact=True)
+    assert rep["boxes"] > 0
     print(rep)
 
 
@@ -74,10 +87,9 @@ def test_legacy_stage1_kernel(ws, cascade, monkeypatch):
     form; selected by CCNN_S1_LEGACY=1 at ccnn_create) on the ragged multi-frame batch."""
     monkeypatch.setenv("CCNN_S1_LEGACY", "1")
     fr = synth_frames.make_stills(3, 333, 257, 991, 20)
-    T1 = quantile_T1(cascade, fr, 20, 1.1, 0.995)
-    T2 = (0.8, 0.1)
+    T1, T2 = exact(cascade, fr, 20, 1.1, 0.995, Tnn=1)
     det = make_det(ws, T1, T2, 1, 0)
-    rep = parity.compare_run(det, cascade, fr, 20, 1.1, T1, T2, 1, 0)
+    rep = parity.compare_run(det, cascade, fr, 20, 1.1, T1, T2, 1, 0, expect_exact=True)
     print(rep)
 
 
@@ -85,11 +97,10 @@ def test_fddb_like_stills(ws, cascade):
     """C2 settings (minSize 15, scaleFactor 1.05: 67 levels) on 2 of the 450x450 stills."""
     c = configs.C2
     fr = c.make_frames(2)
-    T1 = quantile_T1(cascade, fr, c.min_face, c.scale_step, 0.9995)
-    T2 = (0.9, 0.2)
+    T1, T2 = exact(cascade, fr, c.min_face, c.scale_step, 0.9995, Tnn=c.Tnn)
     det = make_det(ws, T1, T2, c.Tnn, c.rule)
     rep = parity.compare_run(det, cascade, fr, c.min_face, c.scale_step, T1, T2, c.Tnn, c.rule,
-                             check_levels=True)
+                             check_levels=True, expect_exact=True)
     print(rep)
 
 
@@ -136,23 +147,33 @@ def test_c4_full_size_bench_config(ws, cascade):
         assert ((f, l, i, j) in gset) == (np.float32(s1) > np.float32(T1))
         n_checked += 1
     assert n_checked > 2900
-    # near-threshold windows must be the only possible disagreements: full oracle on 2 frames
-    for f in (0, len(fr) - 1):
-        oc, ob, os_ = oracle.detect(cascade, fr[f:f + 1], c.min_face, c.scale_step, T1, T2, c.Tnn,
-                                    c.rule)
-        oset = {(f, int(k["level"]), int(k["iy"]), int(k["ix"])) for k in oc}
-        gf = {k for k in gset if k[0] == f}
-        diff = oset ^ gf
-        for (_, l, i, j) in diff:
-            s1 = oracle.stage1_window(cascade.nets[0], level(f, l), i, j)
-            assert abs(s1 - T1) <= parity.TOL
-        if not diff and not any(np.any(np.abs(k["r2"] - T2[0]) <= parity.TOL) or
-                                np.any(np.abs(k["r3"] - T2[1]) <= parity.TOL) for k in oc):
-            gb = sorted((int(b["x"]), int(b["y"]), int(b["w"]), int(b["h"]), int(b["neighbors"]))
-                        for b in boxes[boxes["frame"] == f])
-            obx = sorted((int(b["x"]), int(b["y"]), int(b["w"]), int(b["h"]), int(b["neighbors"]))
-                         for b in ob)
-            assert gb == obx
+    # every frame's NMS vs the oracle's grouping of the GPU's own accepted boxes (exact), and
+    # the first / last frame in full vs the oracle (boxes of every frame compared, exempt
+    # decisions taken as the GPU's)
+    parity.check_nms(cands, boxes, len(fr))
+    rep = _full_frames_vs_oracle(cascade, fr, cands, boxes, c, T1, T2, (0, len(fr) - 1))
+    assert rep["frames_boxes_checked"] == 2
+    print(rep)
+
+
+def _full_frames_vs_oracle(cascade, fr, cands, boxes, c, T1, T2, frame_ids):
+    """Survivors, selective outcome and final boxes of whole frames of a full-size batch vs
+    oracle.detect of those frames (tests/parity.py check_selective_and_boxes)."""
+    lv = oracle.level_table(fr.shape[2], fr.shape[1], c.min_face, c.scale_step)
+    lvs = [lv] * len(fr)
+    ex = parity.exempt_windows(cascade, fr, lvs, T1, frame_ids)
+    rep = parity.Report()
+    for f in frame_ids:
+        oc, ob, _ = oracle.detect(cascade, fr[f:f + 1], c.min_face, c.scale_step, T1, T2, c.Tnn,
+                                  c.rule)
+        oc["frame"] = f
+        ob["frame"] = f
+        parity.check_selective_and_boxes(cands[cands["frame"] == f], boxes[boxes["frame"] == f],
+                                         None, oc, ob, None, {k for k in ex if k[0] == f}, fr,
+                                         lvs, cascade, T1, T2, c.Tnn, c.rule, frame_ids=[f],
+                                         rep=rep)
+    rep["exempt_T1"] = len(ex)
+    return rep
 
 
 def _sampled_full_size(ws, cascade, c, n_cands, n_windows, full_frames, queue_capacity=4096):
@@ -208,48 +229,41 @@ def _sampled_full_size(ws, cascade, c, n_cands, n_windows, full_frames, queue_ca
         assert ((f, l, i, j) in gset) == (np.float32(s1) > np.float32(T1))
         n_checked += 1
     assert n_checked > 0.95 * n_windows
-    for f in full_frames:
-        oc, ob, _ = oracle.detect(cascade, fr[f:f + 1], c.min_face, c.scale_step, T1, T2, c.Tnn, c.rule)
-        oset = {(f, int(k["level"]), int(k["iy"]), int(k["ix"])) for k in oc}
-        diff = oset ^ {k for k in gset if k[0] == f}
-        for (_, l, i, j) in diff:
-            assert abs(oracle.stage1_window(cascade.nets[0], level(f, l), i, j) - T1) <= parity.TOL
-        if not diff and not any(np.any(np.abs(k["r2"] - T2[0]) <= parity.TOL) or
-                                np.any(np.abs(k["r3"] - T2[1]) <= parity.TOL) for k in oc):
-            gb = sorted((int(b["x"]), int(b["y"]), int(b["w"]), int(b["h"]), int(b["neighbors"]))
-                        for b in boxes[boxes["frame"] == f])
-            obx = sorted((int(b["x"]), int(b["y"]), int(b["w"]), int(b["h"]), int(b["neighbors"]))
-                         for b in ob)
-            assert gb == obx
+    nf, n_raw = parity.check_nms(cands, boxes, len(fr))
+    assert nf == len(fr)
+    rep = _full_frames_vs_oracle(cascade, fr, cands, boxes, c, T1, T2, full_frames)
+    assert rep["frames_boxes_checked"] == len(full_frames)
+    print("nms raw boxes", n_raw, "full frames", rep)
     return len(cands), checked_sel
 
 
 def test_c5_full_size_clutter_sampled(ws, cascade):
     """C5: 16 cluttered 4K frames at ~1% stage-1 survival (~50k survivors, the selective-unit
-    and NMS stress), queue capacity as in bench.py."""
-    n, k = _sampled_full_size(ws, cascade, configs.C5, 300, 2000, [0], queue_capacity=40000)
+    and NMS stress; ~1,000 raw boxes per frame), queue capacity as in bench.py: every frame's
+    NMS exact vs or_group of the GPU's accepted boxes, every frame's boxes vs oracle.detect."""
+    n, k = _sampled_full_size(ws, cascade, configs.C5, 300, 2000, range(16), queue_capacity=40000)
     assert n > 10000
     print(n, k)
 
 
 def test_c2_full_size_fddb_sampled(ws, cascade):
     """C2: 256 FDDB-like 450x450 stills, min face 15 (upscaled levels), scale 1.05."""
-    n, k = _sampled_full_size(ws, cascade, configs.C2, 300, 3000, [0, 255])
+    n, k = _sampled_full_size(ws, cascade, configs.C2, 300, 3000, list(range(0, 256, 4)) + [255])
     print(n, k)
 
 
 def test_c4_full_size_selective_all_survivors(ws, cascade):
     """C4 (the bench workload): every stage-1 survivor through the oracle's selective unit
-    (K2, K3, delta, score, raw box), plus sampled windows and the full oracle boxes of the
-    first frame."""
-    n, k = _sampled_full_size(ws, cascade, configs.C4, 100000, 2000, [0])
+    (K2, K3, delta, score, raw box), plus sampled windows and every frame's boxes vs the
+    full oracle."""
+    n, k = _sampled_full_size(ws, cascade, configs.C4, 100000, 2000, range(32))
     assert k >= 0.9 * n
     print(n, k)
 
 
 def test_c3_full_size_1080p_sampled(ws, cascade):
     """C3: a batch of 1080p video frames, min face 40, scale 1.2."""
-    n, k = _sampled_full_size(ws, cascade, configs.C3, 300, 3000, [0])
+    n, k = _sampled_full_size(ws, cascade, configs.C3, 300, 3000, range(32))
     print(n, k)
 
 
@@ -370,28 +384,47 @@ def test_streaming_submit_collect(ws):
     assert np.array_equal(got[5], ref[1])
 
 
-def test_streaming_device_frames_overlapped_pyramid(ws):
+def test_streaming_device_frames_overlapped_pyramid(ws, cascade):
     """The bench's path: device-resident batches, three in flight, so batch k+2's pyramid (own
-    stream, own level arena) overlaps batch k's stage 1 .. NMS: results equal the synchronous
-    ccnn_detect of each batch, in order (C4 4K frames, distinct content per batch)."""
+    stream, own level arena) overlaps batch k's stage 1 .. NMS.  Every collected batch equals
+    oracle.detect of its frames (survivors, selective outcome, every frame's boxes, Table-1
+    counts; thresholds placed with a margin on these frames, so nothing is exempt) and the
+    synchronous ccnn_detect of the same batch (C4 4K frames, distinct content per batch;
+    P:127 "CNN1 moves to the next level regardless", S:426 mode equivalence)."""
     import torch
     c = configs.C4
-    T1, T2 = c.thresholds()
-    batches = [torch.from_numpy(c.make_frames(4, seed=configs.FRAME_SEED + 13 * k)).cuda()
-               for k in range(5)]
+    host = [c.make_frames(3, seed=configs.FRAME_SEED + 13 * k) for k in range(5)]
+    allf = np.concatenate(host)
+    T1, T2 = exact(cascade, allf, c.min_face, c.scale_step, 1.0 - 2e-4, Tnn=c.Tnn)
+    batches = [torch.from_numpy(h).cuda() for h in host]
     det = make_det(ws, T1, T2, c.Tnn, c.rule, max_batch=4)
-    ref = [det.detect(b, c.min_face, c.scale_step) for b in batches]
     got = []
+
+    def collect():
+        b = det.collect()
+        got.append((b, det.candidates(), dict(det.last_stats)))
     det.submit(batches[0], c.min_face, c.scale_step)
     det.submit(batches[1], c.min_face, c.scale_step)
     for k in range(2, len(batches)):                  # three in flight
         det.submit(batches[k], c.min_face, c.scale_step)
-        got.append(det.collect())
-    got.append(det.collect())
-    got.append(det.collect())
-    for k in range(len(batches)):
-        assert np.array_equal(got[k], ref[k]), k
-    assert sum(len(r) for r in ref) > 0
+        collect()
+    collect()
+    collect()
+    lv = oracle.level_table(c.width, c.height, c.min_face, c.scale_step)
+    total = 0
+    for k, (gb, gc, gst) in enumerate(got):
+        fr = host[k]
+        oc, ob, ost = oracle.detect(cascade, fr, c.min_face, c.scale_step, T1, T2, c.Tnn, c.rule)
+        ex = parity.exempt_windows(cascade, fr, [lv] * len(fr), T1)
+        assert not ex
+        rep = parity.check_selective_and_boxes(gc, gb, gst, oc, ob, ost, ex, fr, [lv] * len(fr),
+                                               cascade, T1, T2, c.Tnn, c.rule)
+        assert rep["frames_boxes_checked"] == len(fr) and rep["exempt_T2"] == 0, rep
+        parity.check_nms(gc, gb, len(fr))
+        assert np.array_equal(gb, det.detect(batches[k], c.min_face, c.scale_step)), k
+        total += len(gb)
+        print(k, rep)
+    assert total > 0
 
 
 @pytest.mark.parametrize("seg", [1, 3, 7])
@@ -401,9 +434,10 @@ def test_segment_heights_and_patchwork(ws, cascade, seg):
     stage-1 maps and survivors still match the oracle."""
     c = configs.C3
     fr = c.make_frames(1)
-    T1 = quantile_T1(cascade, fr, 96, 1.25, 0.999)
-    det = make_det(ws, T1, (0.9, 0.2), 2, 0, max_batch=2, segment_rows=seg)
-    rep = parity.compare_run(det, cascade, fr, 96, 1.25, T1, (0.9, 0.2), 2, 0, check_levels=False)
+    T1, T2 = exact(cascade, fr, 96, 1.25, 0.999)
+    det = make_det(ws, T1, T2, 2, 0, max_batch=2, segment_rows=seg)
+    rep = parity.compare_run(det, cascade, fr, 96, 1.25, T1, T2, 2, 0, check_levels=False,
+                             expect_exact=True)
     assert rep["survivors"] > 10
     print(rep)
 
@@ -426,11 +460,10 @@ def _mixed_frames():
 
 def test_mixed_size_frames_parity(ws, cascade):
     fr = _mixed_frames()
-    T1 = _quantile_T1_list(cascade, fr, 20, 1.15, 0.995)
-    T2 = (0.8, 0.1)
+    T1, T2 = exact(cascade, fr, 20, 1.15, 0.995, Tnn=1)
     det = make_det(ws, T1, T2, 1, 0, max_w=640, max_h=480, max_batch=8)
-    rep = parity.compare_run(det, cascade, fr, 20, 1.15, T1, T2, 1, 0)
-    assert rep["survivors"] > 50
+    rep = parity.compare_run(det, cascade, fr, 20, 1.15, T1, T2, 1, 0, expect_exact=True)
+    assert rep["survivors"] > 50 and rep["frames_boxes_checked"] == len(fr)
     print(rep)
 
 
