@@ -2,8 +2,12 @@
 
 Contract:
   python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config c4]
-  N > 1: launched by torchrun, one rank per GPU, frames sharded by rank (weak scaling);
-  NCCL is used once, for the final all_gather of the detections.
+  N > 1: one rank per GPU (under torchrun, or spawned by bench.py itself through
+  torch.distributed.run when WORLD_SIZE is unset); the global stream of N x batch frames is
+  sharded by frame (rank r owns frames g = r mod N: weak scaling); the only collective is
+  the final all_gather of the detections (NCCL; gloo when ranks share a GPU, e.g.
+  --dist-backend gloo on a 1-GPU box), and rank 0 checks the merged boxes bit for bit
+  against a 1-rank detection of the same global frames.
 A step = one batch of synthetic frames through the public API (ccnn_submit + ccnn_collect,
 three batches in flight; pyramid -> fused stage 1 -> selective unit -> NMS -> boxes on the host).  `value` is timed with CUDA events on the
 ctx stream with the batch already resident in HBM (265 MB of 4K frames per step, larger
@@ -132,7 +136,7 @@ def parse_cpulist(text):
 def bind_host_to_gpu(dev_index):
     """Pin this process to the CPUs of the GPU's NUMA node (so the pinned host frames are
     allocated on the node whose PCIe root hosts the GPU: the H2D of e2e then does not cross the
-    socket interconnect).  Returns the previous affinity, or None if the topology is unknown."""
+    socket interconnect).  Returns (previous affinity or None, outcome text)."""
     try:
         import torch
         uuid = str(torch.cuda.get_device_properties(dev_index).uuid)
@@ -145,12 +149,14 @@ def bind_host_to_gpu(dev_index):
             cpus = parse_cpulist(f.read())
         old = os.sched_getaffinity(0)
         use = cpus & old
-        if not use or use == old:
-            return None
+        if not use:
+            return None, f"not bound: GPU {bus} local CPUs outside this process's affinity"
+        if use == old:
+            return None, f"not bound: all {len(old)} usable CPUs are local to GPU {bus}"
         os.sched_setaffinity(0, use)
-        return old
-    except Exception:
-        return None
+        return old, f"bound to the {len(use)} CPUs local to GPU {bus}"
+    except Exception as e:
+        return None, f"not bound: topology unknown ({type(e).__name__})"
 
 
 def measured_peaks():
@@ -161,24 +167,103 @@ def measured_peaks():
         return {}
 
 
-def cpu_baseline(cfg, cascade_ws, frames, T1, T2, budget_s=20.0):
-    """The oracle as it stands, on this host's cores, on a bounded sample of the workload."""
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_baseline(cfg, cascade_ws, frames, T1, T2, budget_s=10.0):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the workload
+    (SURVEY §8(d)): the dense-scan oracle on all cores (`value`), on 1 core, and the
+    per-window oracle (the plain definition) on all cores (one 4K frame) and on 1 core
+    (one C1 320x240 frame: windows/s)."""
     import oracle
-    from synth import arch
+    from synth import arch, configs
     cas = oracle.Cascade(arch.NETS, cascade_ws)
     cores = len(os.sched_getaffinity(0))
-    t0 = time.perf_counter()
-    n = 0
-    while n < len(frames):
-        oracle.detect(cas, frames[n:n + 1], cfg.min_face, cfg.scale_step, T1, T2, cfg.Tnn,
-                      cfg.rule, n_threads=cores)
-        n += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
+
+    def run(frs, dense, threads, c=cfg, budget=None):
+        t0 = time.perf_counter()
+        n = 0
+        while n < len(frs):
+            oracle.detect(cas, frs[n:n + 1], c.min_face, c.scale_step, T1, T2, c.Tnn, c.rule,
+                          dense=dense, n_threads=threads)
+            n += 1
+            if budget is None or time.perf_counter() - t0 > budget:
+                break
+        return n, time.perf_counter() - t0
+
+    n, dt = run(frames, True, cores, budget=budget_s)
+    n1, dt1 = run(frames, True, 1)
+    npw, dtpw = run(frames, False, cores)
+    c1 = configs.C1
+    f1 = c1.make_frames(1)
+    lv1 = oracle.level_table(c1.width, c1.height, c1.min_face, c1.scale_step)
+    w1 = sum(oracle.window_grid(w, h)[0] * oracle.window_grid(w, h)[1] for _, w, h in lv1)
+    _, dtc1 = run(f1, False, 1, c=c1)
+    wpf = sum(((w - 27) // 4 + 1) * ((h - 31) // 4 + 1) for _, w, h in level_table(
+        cfg.width, cfg.height, cfg.min_face, cfg.scale_step))
     return {"value": n / dt, "unit": "frames/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"{n} of the bench's {cfg.width}x{cfg.height} frames through oracle.detect "
-                      f"(C, fp64, dense stage-1 scan, {cores} threads), {dt:.1f} s"}
+                      f"(C, fp64, dense stage-1 scan, {cores} threads), {dt:.1f} s",
+            "dense_1core": {"value": n1 / dt1, "unit": "frames/s", "cores": 1,
+                            "windows_per_s": wpf * n1 / dt1, "sample": f"{n1} frame, {dt1:.1f} s"},
+            "per_window_all_cores": {"value": npw / dtpw, "unit": "frames/s", "cores": cores,
+                                     "windows_per_s": wpf * npw / dtpw,
+                                     "sample": f"{npw} frame, per-window CNN1 (dense=False), {dtpw:.1f} s"},
+            "per_window_1core_c1": {"value": 1.0 / dtc1, "unit": "frames/s", "cores": 1,
+                                    "windows_per_s": w1 / dtc1,
+                                    "sample": f"1 C1 320x240 frame (min face 24), per-window, {dtc1:.1f} s"}}
+
+
+def ncu_stage1_traffic(cfg_id, batch, seg, timeout=240):
+    """DRAM bytes read + written by ONE stage-1 launch of this workload, measured now by an ncu
+    pass over a probe run of this script (None if ncu is unavailable or fails)."""
+    import csv
+    import io
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "--print-units", "base", "-k", "regex:stage1_tc", "-s", "2",
+           "-c", "1", "--csv", sys.executable, os.path.abspath(__file__), "--probe", "--config",
+           cfg_id, "--batch", str(batch), "--seg", str(seg)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout).stdout
+        rows = list(csv.reader(io.StringIO(out[out.index('"ID"'):])))
+        hdr = rows[0]
+        iname, ival = hdr.index("Metric Name"), hdr.index("Metric Value")
+        m = {r[iname]: float(r[ival].replace(",", "")) for r in rows[1:] if len(r) > ival}
+        return m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"], \
+            "ncu live (dram__bytes_read.sum + dram__bytes_write.sum, one launch, %.3f ms)" % (
+                m.get("gpu__time_duration.sum", 0.0) / 1e6)
+    except Exception as e:
+        return None, "ncu probe failed: %s" % type(e).__name__
+
+
+def probe(args, cfg):
+    """--probe: a few synchronous detects of the workload (the ncu traffic pass runs this)."""
+    import torch
+    from paper_1508_01292_b200 import Detector
+    from synth import arch, weights
+    T1, T2 = cfg.thresholds()
+    batch = args.batch or cfg.batch
+    det = Detector(arch.NETS, weights.make_cascade_weights(), T1, T2, cfg.Tnn, cfg.rule,
+                   max_w=cfg.width, max_h=cfg.height, max_batch=batch,
+                   queue_capacity=40000 if cfg.kind == "clutter" else 4096, segment_rows=args.seg)
+    fr = torch.from_numpy(cfg.make_frames(batch)).cuda()
+    for _ in range(4):
+        det.detect(fr, cfg.min_face, cfg.scale_step)
+    det.close()
+    return 0
 
 
 def run_reference(args, cfg):
@@ -217,6 +302,20 @@ def run_reference(args, cfg):
     return 0
 
 
+def spawn_ranks(args):
+    """--gpus N > 1 without a torchrun environment: launch N ranks of this script through
+    torch.distributed.run on this node (127.0.0.1), pass rank 0's output through."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -226,13 +325,22 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--batch", type=int, default=0, help="frames per step per GPU (0 = config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the live ncu traffic pass")
+    ap.add_argument("--no-verify-merge", action="store_true")
+    ap.add_argument("--dist-backend", default="auto", choices=["auto", "nccl", "gloo"],
+                    help="auto: nccl with one GPU per rank, gloo when ranks share GPUs")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--seg", type=int, default=0, help="stage-1 segment rows (0 = adaptive)")
+    ap.add_argument("--probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     from synth import configs, weights
     cfg = configs.BY_ID[args.config]
+    if args.probe:
+        return probe(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args, cfg)
 
@@ -240,22 +348,39 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = None
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    n_dev = torch.cuda.device_count()
+    dist, backend = None, None
+    torch.cuda.set_device(local % n_dev)
+    dev = torch.device("cuda", torch.cuda.current_device())
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.device("cuda", torch.cuda.current_device())
+        backend = args.dist_backend
+        if backend == "auto":
+            backend = "nccl" if n_dev >= world else "gloo"
+        if backend == "nccl" and n_dev < world:
+            print(f"bench.py: {world} NCCL ranks need {world} GPUs ({n_dev} visible); "
+                  "use --dist-backend gloo to share GPUs", file=sys.stderr)
+            return 2
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    coll_dev = dev if backend == "nccl" else torch.device("cpu")
 
     from paper_1508_01292_b200 import Detector
+    from paper_1508_01292_b200 import dist as cdist
     from synth import arch
     ws = weights.make_cascade_weights()
     T1, T2 = cfg.thresholds()
     batch = args.batch or cfg.batch
-    # frame-sharded weak scaling: rank r owns its own stream segment (frames are independent)
-    frames = cfg.make_frames(batch, seed=configs.FRAME_SEED + 7919 * rank)
+    # frame-sharded weak scaling: the global stream has world x batch frames; rank r owns the
+    # frames g = r mod world (frames are independent, BASELINE north_star)
+    n_global = world * batch
+    my_ids = cdist.shard_frames(n_global, world, rank)
+    frames = cfg.make_frames_at(my_ids, n_global)
     det = Detector(arch.NETS, ws, T1, T2, cfg.Tnn, cfg.rule, max_w=cfg.width, max_h=cfg.height,
                    max_batch=batch, queue_capacity=max(4096, 40000 if cfg.kind == "clutter" else 0),
                    segment_rows=args.seg, device=dev.index)
@@ -270,6 +395,13 @@ def main():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], device=coll_dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     for _ in range(args.warmup):
         det.detect(dframes, cfg.min_face, cfg.scale_step)
@@ -299,22 +431,18 @@ def main():
         mma_flops += stats["s1_mma_flops"]
         launches += stats["kernel_launches"]
         all_boxes.append(b)
-    # the only cross-GPU exchange: gather every rank's detections (NCCL), once
+    # the only cross-GPU exchange: gather every rank's detections, once
+    merged = None
     if dist is not None:
-        from paper_1508_01292_b200 import dist as cdist
-        ids = cdist.shard_frames(batch * world, world, rank)      # this rank's global frames
-        merged = cdist.gather_boxes(cdist.to_global(all_boxes[-1], ids), device=dev)
+        merged = cdist.gather_boxes(cdist.to_global(all_boxes[-1], my_ids),
+                                    device=dev if backend == "nccl" else None)
     e1.record(stream)
     e1.synchronize()
     barrier()
-    ms = e0.elapsed_time(e1)
-    if dist is not None:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1))
 
     # ---- e2e: the streaming public API (ccnn_submit / ccnn_collect) with the frames in
-    #      pinned HOST memory: every step copies its 265 MB H2D and reads its boxes back;
+    #      pinned HOST memory: every step copies its frames H2D and reads its boxes back;
     #      the copy of step k+1 overlaps the kernels of step k (three batches in flight) ----
     # enough steps for a >= ~100 ms e2e region (host jitter of a few ms must not dominate a
     # small config's rate): estimate a step from the device-timed loop + H2D at ~40 GB/s
@@ -327,7 +455,7 @@ def main():
         det.detect(dframes, cfg.min_face, cfg.scale_step)
         alone.append(det.last_stats["ms"])
     alone = [float(x) for x in np.median(np.array(alone), axis=0)]
-    old_aff = bind_host_to_gpu(dev.index)
+    old_aff, numa = bind_host_to_gpu(dev.index)
     host = torch.from_numpy(frames).pin_memory()
     det.detect(host, cfg.min_face, cfg.scale_step)
     barrier()
@@ -344,16 +472,56 @@ def main():
     h1.record(stream)
     h1.synchronize()
     barrier()
-    ms_e2e = max(h0.elapsed_time(h1), 1000.0 * (time.perf_counter() - t_e2e0) - 1.0)
+    ms_e2e = max_over_ranks(max(h0.elapsed_time(h1), 1000.0 * (time.perf_counter() - t_e2e0) - 1.0))
     clk = clocks.stop() if clocks else None     # device-timed + e2e regions (both under load)
-    numa = None
+    # pure H2D rate of these pinned frames on this box (the e2e path's bound at 4K)
+    hbuf = torch.empty_like(dframes)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    for _ in range(3):
+        hbuf.copy_(host, non_blocking=True)
+    c1.record(stream)
+    c1.synchronize()
+    h2d_gbs = 3 * frames.nbytes / (c0.elapsed_time(c1) / 1000.0) / 1e9
+    del hbuf
     if old_aff is not None:
-        numa = f"host pinned to the GPU's NUMA node ({len(os.sched_getaffinity(0))} CPUs)"
         os.sched_setaffinity(0, old_aff)
-    if dist is not None:
-        t = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+
+    # ---- batch-1 latency: one frame per synchronous ccnn_detect (device-resident frame) ----
+    lat_wall, lat_dev = [], []
+    one = dframes[:1]
+    for k in range(23):
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        q0.record(stream)
+        det.detect(one, cfg.min_face, cfg.scale_step)
+        q1.record(stream)
+        q1.synchronize()
+        if k >= 3:
+            lat_wall.append(1000.0 * (time.perf_counter() - t0))
+            lat_dev.append(q0.elapsed_time(q1))
+
+    # ---- merged detections vs a 1-rank run over the same global frames (bit for bit) ----
+    merge_check = None
+    if dist is not None and not args.no_verify_merge:
+        ok = None
+        if rank == 0:
+            ref = []
+            for g0 in range(0, n_global, batch):
+                ids = np.arange(g0, min(n_global, g0 + batch))
+                fr = torch.from_numpy(cfg.make_frames_at(ids, n_global)).to(dev)
+                ref.append(cdist.to_global(det.detect(fr, cfg.min_face, cfg.scale_step), ids))
+            ref = cdist.sort_boxes(np.concatenate(ref))
+            ok = bool(len(ref) == len(merged) and ref.tobytes() == merged.tobytes())
+            merge_check = {"global_frames": n_global, "merged_boxes": int(len(merged)),
+                           "reference": "1-rank ccnn_detect of the same global frames on rank 0",
+                           "bit_exact": ok}
+        barrier()
+
+    traffic, traffic_src = None, "not measured (--no-traffic)"
+    if rank == 0 and world == 1 and not args.no_traffic:
+        traffic, traffic_src = ncu_stage1_traffic(args.config, batch, args.seg)
 
     if rank == 0:
         total_frames = world * batch * args.steps
@@ -365,17 +533,9 @@ def main():
         fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12     # FFMA pipe peak
         # stage 1 runs its three conv layers as fp16 tcgen05 MMAs (exact pixels, hi+lo split
         # weights / activations, fp32 accumulators): the dense fp16 tensor peak binds.  The
-        # kernel is timed inside a long step -> the sustained measured figure (bf16 and fp16
-        # share the nominal rate, B200_PROFILING.md)
-        tc_peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 2250.0)))
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", "stage1_traffic.json")
-        if os.path.exists(tpath):
-            try:
-                traffic = json.load(open(tpath)).get("bytes_per_launch_per_frame")
-                traffic = traffic * batch if traffic else None
-            except Exception:
-                traffic = None
+        # timed region is short (~15 ms) and runs at the max SM clock (clocks below), so the
+        # burst figure applies (bf16 and fp16 share the nominal rate, B200_PROFILING.md)
+        tc_peak = float(peaks.get("bf16_tflops", 2250.0))
         line = {
             "metric": "4K UHD frames/s (min face 60px)",
             "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
@@ -386,6 +546,7 @@ def main():
                        "H": cfg.height, "min_face": cfg.min_face, "scale_step": cfg.scale_step,
                        "Tnn": cfg.Tnn, "levels": len(levels), "windows_per_frame": windows_per_frame,
                        "parallelism": f"frame-sharded dp{world}",
+                       "dist_backend": backend, "ranks_per_gpu": (world + n_dev - 1) // n_dev if world > 1 else 1,
                        "l2": "inputs larger than L2 (%.0f MB frames/step/GPU)" % (frames.nbytes / 1e6)},
             "stage1_gwindows_per_s": windows_per_frame * batch / (s1_avg_ms / 1000.0) / 1e9 * world,
             "pipeline_gwindows_per_s": windows_per_frame * total_frames / (ms / 1000.0) / 1e9,
@@ -398,12 +559,15 @@ def main():
             "table1_counts_last_step": {k: stats[k] for k in ("windows", "stage1", "stage2", "stage3", "nms")},
             "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tc_peak,
                          "unit": "TFLOP/s", "frac": achieved_tflops / tc_peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "algorithmic_bytes": int(batch * sum(((w + 15) // 16 * 16) * h for _, w, h in levels)),
                          "kernel": "stage1_tc_kernel",
-                         "peak_note": "dense fp16/bf16 tensor peak, measured sustained "
-                                      "(MEASURED_PEAKS.json bf16_tflops_sustained); achieved = "
-                                      "ALGORITHMIC fp32-equivalent FLOPs of CNN1 / measured stage-1 time. "
-                                      "The MMAs actually issued (mma_issued_*) are ~6x that (hi+lo splits, "
-                                      "implicit-GEMM zero taps; DESIGN.md K2); ncu: tc pipe ~80% busy",
+                         "peak_note": "dense fp16/bf16 tensor peak, measured burst "
+                                      "(MEASURED_PEAKS.json bf16_tflops; the ~15 ms timed region runs at "
+                                      "the max SM clock); achieved = ALGORITHMIC fp32-equivalent FLOPs of "
+                                      "CNN1 / measured stage-1 time. The MMAs actually issued "
+                                      "(mma_issued_*) are several times that (hi+lo splits, implicit-GEMM "
+                                      "zero taps; DESIGN.md K2)",
                          "fp32_ffma_peak": fp32_peak,
                          "frac_of_fp32_ffma_peak": achieved_tflops / fp32_peak,
                          # the tensor work the kernel actually issues (all MMAs, zero taps and
@@ -413,10 +577,18 @@ def main():
                          "mma_issued_frac": mma_flops / (s1_ms / 1000.0) / 1e12 / tc_peak if s1_ms > 0 else None},
             "e2e": {"value": world * batch * e2e_steps / (ms_e2e / 1000.0), "unit": "frames/s",
                     "h2d_bytes_per_step": int(frames.nbytes), "d2h_bytes_per_step": int(d2h // e2e_steps),
-                    "host_numa": numa},
+                    "h2d_gbs_achieved": int(frames.nbytes) * e2e_steps / (ms_e2e / 1000.0) / 1e9,
+                    "h2d_gbs_copy_alone": h2d_gbs, "host_numa": numa},
+            "latency_batch1_ms": {"wall_median": float(np.median(lat_wall)),
+                                  "wall_p90": float(np.percentile(lat_wall, 90)),
+                                  "device_median": float(np.median(lat_dev)),
+                                  "call": "synchronous ccnn_detect of 1 device-resident frame"},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
+        if merge_check is not None:
+            line["merge_check"] = merge_check
+        # SURVEY §8(d) / the bench contract: the oracle baseline on rank 0 at N=1 only
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(cfg, ws, frames, T1, T2)
         print(json.dumps(line), flush=True)

@@ -10,6 +10,8 @@ import json
 import os
 from dataclasses import dataclass
 
+import numpy as np
+
 from . import frames
 
 CALIB_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "calib")
@@ -36,6 +38,15 @@ class Config:
             return frames.make_stills(n, self.width, self.height, seed, self.min_face)
         return frames.make_video(n, self.width, self.height, seed, self.min_face,
                                  clutter=(self.kind == "clutter"))
+
+    def make_frames_at(self, indices, n_total, seed=FRAME_SEED):
+        """Frames `indices` of the n_total-frame workload make_frames(n_total) returns (the
+        shard of one rank: frame g of the global stream, identical bytes)."""
+        if self.kind == "stills":
+            return np.stack([frames.make_still(self.width, self.height, seed + int(g), self.min_face)
+                             for g in indices])
+        return frames.make_video_frames(indices, n_total, self.width, self.height, seed,
+                                        self.min_face, clutter=(self.kind == "clutter"))
 
     def thresholds(self):
         with open(os.path.join(CALIB_DIR, self.calib + ".json")) as f:

@@ -127,5 +127,20 @@ def make_video(n: int, w: int, h: int, seed: int, min_face: int, n_faces: int = 
     return out
 
 
+def make_video_frames(indices, n_total: int, w: int, h: int, seed: int, min_face: int,
+                      n_faces: int = 12, clutter: bool = False) -> np.ndarray:
+    """Frames `indices` of the n_total-frame stream make_video(n_total, ...) would return
+    (a rank's shard of a stream: identical bytes, without materialising the other frames)."""
+    cw, ch = w + 2 * n_total, h + n_total
+    canvas = make_still(cw, ch, seed, min_face, n_faces=n_faces, clutter=clutter)
+    idx = [int(f) for f in indices]
+    out = np.empty((len(idx), h, w), np.uint8)
+    for k, f in enumerate(idx):
+        if not 0 <= f < n_total:
+            raise ValueError("frame index out of range")
+        out[k] = canvas[f:f + h, 2 * f:2 * f + w]
+    return out
+
+
 def make_stills(n: int, w: int, h: int, seed: int, min_face: int) -> np.ndarray:
     return np.stack([make_still(w, h, seed + k, min_face) for k in range(n)])
