@@ -72,7 +72,7 @@ def _build(force, verbose, extra, objname):
 
 if __name__ == "__main__":
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
-    if args:   # python build.py <variant> DEFINE1 DEFINE2 ...
-        build(variant=args[0], defines=args[1:])
+    if args:   # python build.py <variant> DEFINE1[,DEFINE2 ...] ...
+        build(variant=args[0], defines=[d for a in args[1:] for d in a.split(",") if d])
     else:
         build(force="--force" in sys.argv, verbose=True)

@@ -30,11 +30,12 @@ struct PyrTile {
     int xo, y_beg, nr;     // output column, first row, rows of this tile (<= kPyrTileRows)
 };
 
-// decode this CTA's tile; false if the thread has no column
+// decode this CTA's tile (descriptor `first` + blockIdx.x of the frame's list); false if the
+// thread has no column
 __device__ __forceinline__ bool pyr_tile(const FrameInfo& F, const LevelInfo* __restrict__ lv,
-                                         const uint32_t* __restrict__ tiles, PyrTile& T)
+                                         const uint32_t* __restrict__ tiles, int first, PyrTile& T)
 {
-    const uint32_t d = __ldg(tiles + F.tile_off + blockIdx.x);
+    const uint32_t d = __ldg(tiles + F.tile_off + first + blockIdx.x);
     T.L = lv + F.level0 + (int)(d & 0xFFu);
     T.xo = (int)((d >> 8) & 0xFFu) * kPyrCols + threadIdx.x;
     T.y_beg = (int)(d >> 16) * kPyrTileRows;
@@ -42,12 +43,13 @@ __device__ __forceinline__ bool pyr_tile(const FrameInfo& F, const LevelInfo* __
     return T.xo < T.L->pitch;
 }
 
-// p0*(2048-a) + p1*a == (p0 << 11) + (p1 - p0)*a, exactly (O2)
+// O2: ((p00 (2048-ax) + p01 ax) (2048-ay) + (p10 (2048-ax) + p11 ax) ay + 2^21) >> 22, as
+// 6 integer multiply-adds (every partial sum < 2^31)
 __device__ __forceinline__ uint8_t blend(int p00, int p01, int p10, int p11, int ax, int ay)
 {
-    const int top = (p00 << 11) + (p01 - p00) * ax;
-    const int bot = (p10 << 11) + (p11 - p10) * ax;
-    return (uint8_t)(((top << 11) + (bot - top) * ay + (1 << 21)) >> 22);
+    const int top = p00 * (2048 - ax) + p01 * ax;
+    const int bot = p10 * (2048 - ax) + p11 * ax;
+    return (uint8_t)((top * (2048 - ay) + bot * ay + (1 << 21)) >> 22);
 }
 
 // the y-table entries of a row group: 16-B loads (the table is padded and aligned,
@@ -123,20 +125,22 @@ __device__ __forceinline__ void quad_tile(const FrameInfo& F, const LevelInfo& L
     }
 }
 
-// the tiles of the levels with sigma >= kQuadSigma (the other tiles exit at once)
+// the quad class: the tiles of the levels with sigma >= kQuadSigma (the last class of the list)
 __global__ void __launch_bounds__(kPyrCols) pyramid_quad_kernel(
     const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
     const LevelInfo* __restrict__ lv, const uint32_t* __restrict__ tiles,
     const uint32_t* __restrict__ tabs)
 {
     const FrameInfo F = frames[blockIdx.y];
-    if ((int)blockIdx.x >= F.tiles) return;
-    const uint32_t d = __ldg(tiles + F.tile_off + blockIdx.x);
+    const int first = F.tiles_s + F.tiles_g;
+    if ((int)blockIdx.x >= F.tiles - first) return;
+    const uint32_t d = __ldg(tiles + F.tile_off + first + blockIdx.x);
     const LevelInfo& L = lv[F.level0 + (int)(d & 0xFFu)];
-    if (L.sigma < kQuadSigma) return;
     quad_tile(F, L, (int)((d >> 8) & 0xFFu) * kPyrCols, (int)(d >> 16) * kPyrTileRows, levels, tabs);
 }
 
+// the gather class (the tiles after the staged class; every tile of a frame narrower or
+// shorter than 2 px, which has no other class)
 template <bool SAFE>
 __global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
     const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
@@ -144,13 +148,9 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
     const uint32_t* __restrict__ tabs)
 {
     const FrameInfo F = frames[blockIdx.y];
-    if ((int)blockIdx.x >= F.tiles) return;
-    if (SAFE) {                                                  // CTA-uniform: quad tiles
-        const uint32_t d = __ldg(tiles + F.tile_off + blockIdx.x);   // go to pyramid_quad_kernel
-        if (lv[F.level0 + (int)(d & 0xFFu)].sigma >= kQuadSigma) return;
-    }
+    if ((int)blockIdx.x >= F.tiles_g) return;
     PyrTile T;
-    if (!pyr_tile(F, lv, tiles, T)) return;
+    if (!pyr_tile(F, lv, tiles, F.tiles_s, T)) return;
     const LevelInfo& L = *T.L;
     // SAFE (every frame W, H >= 2): the tables encode the edge so that i1 = i0 + 1 always
     // (runtime.cu sample_entry); otherwise the clamped form
@@ -203,6 +203,93 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
     }
 }
 
+// STAGED class (kPyrStagedSigma <= sigma < kQuadSigma: the large levels, ~3/4 of all level
+// pixels at C4): the two source rows of each of the tile's 32 output rows are copied into
+// shared memory as aligned 16-B chunks (cp.async, L2 -> shared memory, no register or L1
+// traffic; one wait + barrier per CTA), then each thread resamples its output column from
+// shared memory: 4 byte reads and the O2 blend in 6 integer multiply-adds per pixel, instead of
+// 4 L1 gathers with 64-bit address arithmetic.  Frames whose data or pitch are not 16-B
+// aligned (a device view of a pitched buffer) take the byte-gather form for the same tile.
+constexpr int kStgRS = ((int)(kPyrCols / kPyrStagedSigma) + 2 + 15 + 15) / 16 * 16;  // row bytes
+constexpr int kStgSmem = 2 * kPyrTileRows * kStgRS;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+}
+
+__global__ void __launch_bounds__(kPyrCols) pyramid_staged_kernel(
+    const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
+    const LevelInfo* __restrict__ lv, const uint32_t* __restrict__ tiles,
+    const uint32_t* __restrict__ tabs)
+{
+    extern __shared__ __align__(16) uint8_t stg[];
+    const FrameInfo F = frames[blockIdx.y];
+    if ((int)blockIdx.x >= F.tiles_s) return;
+    const uint32_t d = __ldg(tiles + F.tile_off + blockIdx.x);
+    const LevelInfo& L = lv[F.level0 + (int)(d & 0xFFu)];
+    const int pitch = L.pitch;
+    const int tx0 = (int)((d >> 8) & 0xFFu) * kPyrCols;
+    const int ty0 = (int)(d >> 16) * kPyrTileRows;
+    const int nr = min(kPyrTileRows, L.lh - ty0);
+    const uint32_t* __restrict__ xt = tabs + L.tab_off;
+    const uint32_t* __restrict__ yt = xt + pitch + ty0;       // padded: 32 entries
+    const int xo = tx0 + (int)threadIdx.x;
+    if (((uintptr_t)F.data | (uintptr_t)F.pitch) & 15u) {      // unaligned rows: byte gathers
+        if (xo >= pitch) return;
+        const uint32_t e = __ldg(xt + xo);
+        const uint8_t* col = F.data + (e & 0xFFFFu);
+        const int ax = (int)(e >> 16);
+        uint8_t* dst = levels + L.offset + xo + (int64_t)ty0 * pitch;
+        for (int r = 0; r < nr; ++r) {
+            const uint32_t ye = __ldg(yt + r);
+            const uint8_t* r0 = col + (int64_t)(ye & 0xFFFFu) * F.pitch;
+            dst[(int64_t)r * pitch] = blend(r0[0], r0[1], r0[F.pitch], r0[F.pitch + 1], ax, (int)(ye >> 16));
+        }
+        return;
+    }
+    // source columns of the tile: from x0 of its first column (rounded down to 16 B) to x0 + 1
+    // of its last (x tables are padded to the pitch, monotone)
+    const int xl = min(tx0 + kPyrCols, pitch) - 1;
+    const int xb = (int)(__ldg(xt + tx0) & 0xFFFFu) & ~15;
+    const int nch = ((int)(__ldg(xt + xl) & 0xFFFFu) + 1 - xb) / 16 + 1;   // <= kStgRS / 16
+    const int RS = nch * 16;
+    // shared row 2r + e = source row y0(ty0 + r) + e: warp w copies rows w, w + 4, ..., lane l
+    // its chunks l, l + 32
+    {
+        const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
+        const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stg);
+        const uint8_t* base = F.data + xb;
+        for (int row = warp; row < 2 * nr; row += kPyrCols / 32) {
+            const int gy = (int)(__ldg(yt + (row >> 1)) & 0xFFFFu) + (row & 1);
+            const uint8_t* src = base + (int64_t)gy * F.pitch;
+            const uint32_t dst = sbase + (uint32_t)(row * RS);
+            for (int c = lane; c < nch; c += 32) cp_async16(dst + 16u * c, src + 16 * c);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+    __syncthreads();
+    if (xo >= pitch) return;
+    const uint32_t e = __ldg(xt + xo);
+    const int wb = (int)(e >> 16), wa = 2048 - wb;
+    const uint8_t* s = stg + ((int)(e & 0xFFFFu) - xb);
+    uint8_t* dst = levels + L.offset + xo + (int64_t)ty0 * pitch;
+    for (int g0 = 0; g0 < nr; g0 += kPyrRows) {                // CTA-uniform
+        uint32_t ye[kPyrRows];
+        load_rows(yt + g0, ye);
+#pragma unroll
+        for (int r = 0; r < kPyrRows; ++r) {
+            if (g0 + r < nr) {
+                const uint8_t* s0 = s + (2 * (g0 + r)) * RS;
+                const int wd = (int)(ye[r] >> 16), wc = 2048 - wd;
+                const int top = (int)s0[0] * wa + (int)s0[1] * wb;
+                const int bot = (int)s0[RS] * wa + (int)s0[RS + 1] * wb;
+                dst[(int64_t)(g0 + r) * pitch] = (uint8_t)((top * wc + bot * wd + (1 << 21)) >> 22);
+            }
+        }
+    }
+}
+
 // tld4 (texture gather, red channel) with an integer destination type: the four texels of
 // the 2x2 footprint at unnormalised (u, v) as zero-extended u32 -- order (i0, j1), (i1, j1),
 // (i1, j0), (i0, j0) for the footprint at (i0 + 1, j0 + 1); clamp addressing supplies
@@ -223,7 +310,7 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_tex_kernel(
     const FrameInfo F = frames[blockIdx.y];
     if ((int)blockIdx.x >= F.tiles) return;
     PyrTile T;
-    if (!pyr_tile(F, lv, tiles, T)) return;
+    if (!pyr_tile(F, lv, tiles, 0, T)) return;
     const LevelInfo& L = *T.L;
     const uint32_t e = __ldg(tabs + L.tab_off + T.xo);
     const float u = (float)(e & 0xFFFFu) + 1.0f;
@@ -255,21 +342,39 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_tex_kernel(
 
 }  // namespace
 
-void launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, bool safe,
-                    bool any_quad, bool use_tex, uint8_t* levels, const LevelInfo* d_levels,
-                    const uint32_t* d_tiles, const uint32_t* d_tabs, cudaStream_t s)
+int launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, const int (&max_class)[3],
+                   bool safe, bool use_tex, uint8_t* levels, const LevelInfo* d_levels,
+                   const uint32_t* d_tiles, const uint32_t* d_tabs, cudaStream_t s)
 {
-    if (n_frames <= 0 || max_tiles <= 0) return;
-    const dim3 grid(max_tiles, n_frames);      // frames of other sizes: surplus CTAs exit
-    if (use_tex)
-        pyramid_tex_kernel<<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
-    else if (safe) {
-        pyramid_kernel<true><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
-        if (any_quad)
-            pyramid_quad_kernel<<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
+    if (n_frames <= 0 || max_tiles <= 0) return 0;
+    if (use_tex) {                             // every tile by texture gathers (debug form)
+        pyramid_tex_kernel<<<dim3(max_tiles, n_frames), kPyrCols, 0, s>>>(d_frames, levels, d_levels,
+                                                                          d_tiles, d_tabs);
+        return 1;
     }
-    else
-        pyramid_kernel<false><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
+    int launched = 0;
+    // grid.x = the most tiles any frame has in the class (frames with fewer: surplus CTAs exit)
+    if (max_class[kPyrStaged] > 0) {
+        cudaFuncSetAttribute(pyramid_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kStgSmem);
+        pyramid_staged_kernel<<<dim3(max_class[kPyrStaged], n_frames), kPyrCols, kStgSmem, s>>>(
+            d_frames, levels, d_levels, d_tiles, d_tabs);
+        ++launched;
+    }
+    if (max_class[kPyrGather] > 0) {
+        const dim3 grid(max_class[kPyrGather], n_frames);
+        if (safe)
+            pyramid_kernel<true><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
+        else
+            pyramid_kernel<false><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
+        ++launched;
+    }
+    if (max_class[kPyrQuad] > 0) {
+        pyramid_quad_kernel<<<dim3(max_class[kPyrQuad], n_frames), kPyrCols, 0, s>>>(
+            d_frames, levels, d_levels, d_tiles, d_tabs);
+        ++launched;
+    }
+    return launched;
 }
 
 }  // namespace ccnn

@@ -16,6 +16,7 @@
 #include <tuple>
 #include <functional>
 #include <queue>
+#include <array>
 
 #include "../../include/ccnn.h"
 #include "ccnn_internal.h"
@@ -92,8 +93,9 @@ struct ccnn_ctx {
     int64_t windows_total = 0;
     double s1_mma_flops = 0.0;          // tensor-core FLOPs stage 1 issues for the planned batch
     int pyr_tiles = 0;                  // largest per-frame pyramid tile count
+    int pyr_class_max[3] = {0, 0, 0};   // ... per kernel class (staged, gather, quad)
+    std::vector<int32_t> frame_tiles_s, frame_tiles_g;
     bool all_safe = true;               // every frame W, H >= 2 (pyramid fast path)
-    bool any_quad = false;              // some level has sigma >= kPyrQuadSigma
     std::vector<int32_t> frame_level0, frame_nlevels, frame_tiles, frame_tile_off;
     std::vector<uint32_t> ptiles;       // pyramid tile descriptors (pyramid.cu)
 
@@ -124,7 +126,8 @@ struct ccnn_ctx {
         uint32_t cand_cap = 0;
         int64_t windows = 0;
         double s1_mma_flops = 0.0;
-        bool timed = false, empty = false, quad = false;
+        bool timed = false, empty = false;
+        int pyr_launches = 0;
     } slot[kSlots];
     cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
     cudaStream_t pyr_stream = nullptr;  // pyramids (overlap the previous batch's stage 1..NMS)
@@ -385,14 +388,17 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
     c->frame_tiles.clear();
     c->frame_tile_off.clear();
     c->ptiles.clear();
+    c->frame_tiles_s.clear();
+    c->frame_tiles_g.clear();
     c->pyr_tiles = 0;
+    for (int& m : c->pyr_class_max) m = 0;
     c->all_safe = true;
-    c->any_quad = false;
     const double sf = (double)key.scale_step;
     int64_t off = 0, map_off = 0;
     c->windows_total = 0;
     std::map<std::pair<int, int>, std::vector<int32_t>> tab_cache;   // (W,H) -> tab_off per level
     std::map<std::pair<int, int>, std::pair<int32_t, int32_t>> tile_cache;   // -> (offset, count)
+    std::map<std::pair<int, int>, std::array<int32_t, 3>> class_cache;       // -> count per class
     for (int f = 0; f < (int)key.dims.size(); ++f) {
         const int W = key.dims[f].first, H = key.dims[f].second;
         auto it = tab_cache.find(key.dims[f]);
@@ -416,7 +422,6 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
             L.nx = (lw - kWinW) / kStep + 1;
             L.ny = (lh - kWinH) / kStep + 1;
             L.frame = f;
-            c->any_quad = c->any_quad || s >= kPyrQuadSigma;
             if (have_tabs) {
                 L.tab_off = it->second[k];
             } else {
@@ -438,24 +443,37 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
         }
         c->frame_nlevels.push_back(k);
         // pyramid tile descriptors (level-in-frame | tile column << 8 | tile row << 16),
-        // largest levels first; shared by equally-sized frames
+        // grouped by kernel class (staged | gather | quad), largest levels first within a
+        // class; shared by equally-sized frames
         if (!have_tabs) {
             tab_cache[key.dims[f]] = new_tabs;
-            tile_cache[key.dims[f]] = {(int32_t)c->ptiles.size(), 0};
-            for (int l = 0; l < k && l < 256; ++l) {
-                const LevelInfo& L = c->levels[level0 + l];
-                const int tx_n = (L.pitch + kPyrCols - 1) / kPyrCols;
-                const int ty_n = (L.lh + kPyrTileRows - 1) / kPyrTileRows;
-                for (int ty = 0; ty < ty_n; ++ty)
-                    for (int tx = 0; tx < tx_n; ++tx)
-                        c->ptiles.push_back((uint32_t)l | ((uint32_t)tx << 8) | ((uint32_t)ty << 16));
-            }
-            tile_cache[key.dims[f]].second = (int32_t)c->ptiles.size() - tile_cache[key.dims[f]].first;
+            const int32_t first = (int32_t)c->ptiles.size();
+            int32_t cnt[3] = {0, 0, 0};
+            const bool safe = W >= 2 && H >= 2;
+            for (int cls = 0; cls < 3; ++cls)
+                for (int l = 0; l < k && l < 256; ++l) {
+                    const LevelInfo& L = c->levels[level0 + l];
+                    const int lc = !safe ? kPyrGather : L.sigma >= kPyrQuadSigma ? kPyrQuad
+                                 : L.sigma >= kPyrStagedSigma ? kPyrStaged : kPyrGather;
+                    if (lc != cls) continue;
+                    const int tx_n = (L.pitch + kPyrCols - 1) / kPyrCols;
+                    const int ty_n = (L.lh + kPyrTileRows - 1) / kPyrTileRows;
+                    for (int ty = 0; ty < ty_n; ++ty)
+                        for (int tx = 0; tx < tx_n; ++tx)
+                            c->ptiles.push_back((uint32_t)l | ((uint32_t)tx << 8) | ((uint32_t)ty << 16));
+                    cnt[cls] += tx_n * ty_n;
+                }
+            tile_cache[key.dims[f]] = {first, (int32_t)c->ptiles.size() - first};
+            class_cache[key.dims[f]] = {cnt[0], cnt[1], cnt[2]};
         }
         const auto tc = tile_cache[key.dims[f]];
+        const auto cc = class_cache[key.dims[f]];
         c->frame_tile_off.push_back(tc.first);
         c->frame_tiles.push_back(tc.second);
+        c->frame_tiles_s.push_back(cc[0]);
+        c->frame_tiles_g.push_back(cc[1]);
         c->pyr_tiles = std::max(c->pyr_tiles, tc.second);
+        for (int cls = 0; cls < 3; ++cls) c->pyr_class_max[cls] = std::max(c->pyr_class_max[cls], cc[cls]);
         c->all_safe = c->all_safe && W >= 2 && H >= 2;
     }
     // slack so that the stage-1 loader's last (clamped) word read stays in bounds
@@ -756,7 +774,6 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     sl.windows = ctx->windows_total;
     sl.s1_mma_flops = ctx->s1_mma_flops;
     sl.timed = timed != 0;
-    sl.quad = ctx->all_safe && ctx->any_quad && !(ctx->debug & CCNN_DEBUG_PYR_TEX);
     sl.empty = (L == 0);                           // empty pyramid: not an error
     ctx->last_W = frames[0].w;
     ctx->last_H = frames[0].h;
@@ -908,6 +925,8 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
         fi[f].nlevels = ctx->frame_nlevels[f];
         fi[f].tiles = ctx->frame_tiles[f];
         fi[f].tile_off = ctx->frame_tile_off[f];
+        fi[f].tiles_s = ctx->frame_tiles_s[f];
+        fi[f].tiles_g = ctx->frame_tiles_g[f];
         fi[f].tex = use_tex ? frame_texture(ctx, fi[f].data, fi[f].w, fi[f].h, fi[f].pitch) : 0;
         use_tex = use_tex && fi[f].tex != 0;
     }
@@ -924,9 +943,9 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
         CU(cudaEventCreate(&ctx->epoch));
         CU(cudaEventRecord(ctx->epoch, ps));
     }
-    launch_pyramid(dfi, n, ctx->pyr_tiles, ctx->all_safe, ctx->any_quad, use_tex, sl.arena.as<uint8_t>(),
-                   ctx->d_levels.as<LevelInfo>(), ctx->d_ptiles.as<uint32_t>(),
-                   ctx->d_tabs.as<uint32_t>(), ps);
+    sl.pyr_launches = launch_pyramid(dfi, n, ctx->pyr_tiles, ctx->pyr_class_max, ctx->all_safe, use_tex,
+                                     sl.arena.as<uint8_t>(), ctx->d_levels.as<LevelInfo>(),
+                                     ctx->d_ptiles.as<uint32_t>(), ctx->d_tabs.as<uint32_t>(), ps);
     CU(cudaEventRecord(sl.ev[3], ps));
     // stage 1 on the compute stream once the slot's previous batch has finished with the
     // slot's queue / scratch (its tail) and this batch's pyramid is done
@@ -1014,7 +1033,7 @@ int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_box
         stats->stage2 = hc.n_stage2;
         stats->stage3 = hc.n_stage3;
         stats->nms = hc.n_out;
-        stats->kernel_launches = 4 + (sl.n_jobs ? 1 : 0) + (sl.quad ? 1 : 0);
+        stats->kernel_launches = 3 + sl.pyr_launches + (sl.n_jobs ? 1 : 0);
         stats->s1_mma_flops = sl.s1_mma_flops;
         const int from[5] = {0, 2, 7, 8, 5}, to[5] = {1, 3, 4, 5, 6};
         for (int k = 0; k < 5; ++k) {
