@@ -69,8 +69,8 @@ struct FrameInfo {             // one frame of a batch, as the kernels read it
     int32_t level0, nlevels;   // its levels: LevelInfo[level0 .. level0 + nlevels)
     int32_t tiles, tile_off;   // pyramid tiles of all its levels; their descriptors at
                                // tiles[tile_off ..] (shared by equally-sized frames), in
-                               // kernel classes: [staged | gather | quad]
-    int32_t tiles_s, tiles_g;  // tiles of the staged / gather classes (quad = the rest)
+                               // kernel classes: [gather | quad]
+    int32_t tiles_g, pad_t;    // tiles of the gather class (quad = the rest)
     unsigned long long tex;    // pitch-2D uint8 texture object over data (0 = none)
 };
 struct GrayJob {               // one interleaved R,G,B frame -> its gray copy (ingest.cu)
@@ -99,16 +99,12 @@ struct LevelInfo {             // one pyramid level of one frame of the batch
 #endif
 constexpr int kPyrCols = 128, kPyrRows = PYR_ROWS, kPyrGroups = 32 / PYR_ROWS;
 constexpr int kPyrTileRows = kPyrRows * kPyrGroups;
-// levels with sigma >= kPyrQuadSigma are resampled 4 columns per thread (pyramid_quad_kernel),
-// levels with kPyrStagedSigma <= sigma < kPyrQuadSigma from source rows staged in shared memory
-// (pyramid_staged_kernel), the rest by byte gathers (pyramid_kernel); frames narrower or
-// shorter than 2 px: byte gathers only
+// levels with sigma >= kPyrQuadSigma are resampled 4 adjacent columns per thread
+// (pyramid_quad_kernel), the rest by byte gathers (pyramid_gather4_kernel); frames narrower or
+// shorter than 2 px: the clamped byte-gather form only.  (A third class, source rows staged in
+// shared memory by cp.async for 0.25 <= sigma < 0.7, was measured and removed: DESIGN.md K1.)
 constexpr double kPyrQuadSigma = 0.7;
-#ifndef PYR_STAGED_SIGMA
-#define PYR_STAGED_SIGMA 0.25
-#endif
-constexpr double kPyrStagedSigma = PYR_STAGED_SIGMA;
-enum PyrClass { kPyrStaged = 0, kPyrGather = 1, kPyrQuad = 2 };
+enum PyrClass { kPyrGather = 0, kPyrQuad = 1, kPyrClasses = 2 };
 
 // One stage-1 CTA task: a band of TW = 59 window columns x a segment of rows.  Patchwork
 // (SURVEY §8(f) NEXT #1): a band holds up to kMaxPieces pieces of levels
@@ -165,7 +161,7 @@ void launch_to_gray(const GrayJob* d_jobs, int n_jobs, int sm_count, cudaStream_
 // use_tex: every frame has a texture object (FrameInfo.tex): 2x2 footprints by tex2Dgather
 // max_tiles: the most tiles any frame has, in all classes / per class (PyrClass order);
 // returns the number of kernels launched
-int launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, const int (&max_class)[3],
+int launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, const int (&max_class)[kPyrClasses],
                    bool safe, bool use_tex, uint8_t* levels, const LevelInfo* d_levels,
                    const uint32_t* d_tiles, const uint32_t* d_tabs, cudaStream_t s);
 // stage 1 (fused CNN1 + threshold + compaction): a persistent grid of stage1_grid() CTAs

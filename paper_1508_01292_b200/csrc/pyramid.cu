@@ -9,17 +9,20 @@
 // integer arithmetic.
 //
 // Roofline: HBM-bound in principle (the frame read once + 1 B written per level pixel;
-// DESIGN.md "Roofline"), in practice issue-bound (integer ALU).  grid.y = frame, grid.x =
-// tiles of the frame with the most (surplus CTAs of smaller frames exit).  A CTA owns a
-// tile of 128 consecutive output columns x 32 rows of one level, found through a host-built
-// descriptor (no per-CTA search or division); each thread loads its column's x-table entry
-// once and walks the rows in groups of 8 whose fetches are all issued before any blend;
-// adjacent lanes fetch adjacent output pixels (their frame reads stay within 32/sigma bytes)
-// and store one 32-byte sector per warp-row.
-// Two fetch forms, identical results: four byte gathers (default), or tld4 texture
-// gathers (the 2x2 footprint in one instruction, hardware 2-D addressing -- the paper's
-// texture pyramid) on request (CCNN_DEBUG_PYR_TEX) when every frame has a texture
-// object.  Measured at C4: 0.265 ms byte gathers vs 0.288 ms tld4 (tex_throttle-bound).
+// DESIGN.md K1), in practice bound by the L1 / load-store path of the byte gathers.  Tiles of
+// 128 output columns x 32 rows of one level, described by host-built descriptors grouped by
+// kernel class (runtime.cu build_plan): grid.y = frame, grid.x = the most tiles any frame has
+// in the class (surplus CTAs of smaller frames exit).
+//  * gather class (sigma < 0.7; pyramid_gather4_kernel): warp w owns tile rows 8w .. 8w+7 and
+//    lane l the columns l, l+32, l+64, l+96, so the per-row work (y-table decode, row offset,
+//    weights) is shared by 4 pixels and every store instruction writes 32 consecutive bytes;
+//    16 byte gathers per row are in flight before any blend;
+//  * quad class (sigma >= 0.7, upscaled / mildly scaled levels): 4 adjacent columns per
+//    thread, one 32-bit store per row (pyramid_quad_kernel);
+//  * frames narrower or shorter than 2 px: the clamped form (pyramid_kernel<false>).
+// The O2 blend is 6 integer multiply-adds.  Optional tld4 texture gathers (the 2x2 footprint
+// in one instruction, hardware 2-D addressing -- the paper's texture pyramid) on
+// request (CCNN_DEBUG_PYR_TEX): identical results, measured slower (tex_throttle-bound).
 #include "ccnn_internal.h"
 
 namespace ccnn {
@@ -50,6 +53,13 @@ __device__ __forceinline__ uint8_t blend(int p00, int p01, int p10, int p11, int
     const int top = p00 * (2048 - ax) + p01 * ax;
     const int bot = p10 * (2048 - ax) + p11 * ax;
     return (uint8_t)((top * (2048 - ay) + bot * ay + (1 << 21)) >> 22);
+}
+
+// predicated byte store (the blend above it runs unconditionally: no branch per pixel)
+__device__ __forceinline__ void st_u8_if(uint8_t* p, uint32_t v, bool ok)
+{
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q st.global.u8 [%0], %1; }"
+                 :: "l"(p), "r"(v), "r"((uint32_t)ok) : "memory");
 }
 
 // the y-table entries of a row group: 16-B loads (the table is padded and aligned,
@@ -132,15 +142,15 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_quad_kernel(
     const uint32_t* __restrict__ tabs)
 {
     const FrameInfo F = frames[blockIdx.y];
-    const int first = F.tiles_s + F.tiles_g;
+    const int first = F.tiles_g;
     if ((int)blockIdx.x >= F.tiles - first) return;
     const uint32_t d = __ldg(tiles + F.tile_off + first + blockIdx.x);
     const LevelInfo& L = lv[F.level0 + (int)(d & 0xFFu)];
     quad_tile(F, L, (int)((d >> 8) & 0xFFu) * kPyrCols, (int)(d >> 16) * kPyrTileRows, levels, tabs);
 }
 
-// the gather class (the tiles after the staged class; every tile of a frame narrower or
-// shorter than 2 px, which has no other class)
+// the gather class with clamped sampling (every tile of a frame narrower or shorter than 2 px:
+// its tables do not encode the edge)
 template <bool SAFE>
 __global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
     const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
@@ -150,7 +160,7 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
     const FrameInfo F = frames[blockIdx.y];
     if ((int)blockIdx.x >= F.tiles_g) return;
     PyrTile T;
-    if (!pyr_tile(F, lv, tiles, F.tiles_s, T)) return;
+    if (!pyr_tile(F, lv, tiles, 0, T)) return;
     const LevelInfo& L = *T.L;
     // SAFE (every frame W, H >= 2): the tables encode the edge so that i1 = i0 + 1 always
     // (runtime.cu sample_entry); otherwise the clamped form
@@ -203,89 +213,83 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_kernel(
     }
 }
 
-// STAGED class (kPyrStagedSigma <= sigma < kQuadSigma: the large levels, ~3/4 of all level
-// pixels at C4): the two source rows of each of the tile's 32 output rows are copied into
-// shared memory as aligned 16-B chunks (cp.async, L2 -> shared memory, no register or L1
-// traffic; one wait + barrier per CTA), then each thread resamples its output column from
-// shared memory: 4 byte reads and the O2 blend in 6 integer multiply-adds per pixel, instead of
-// 4 L1 gathers with 64-bit address arithmetic.  Frames whose data or pitch are not 16-B
-// aligned (a device view of a pitched buffer) take the byte-gather form for the same tile.
-constexpr int kStgRS = ((int)(kPyrCols / kPyrStagedSigma) + 2 + 15 + 15) / 16 * 16;  // row bytes
-constexpr int kStgSmem = 2 * kPyrTileRows * kStgRS;
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src)
+// Thread mapping of the gather kernel (SAFE tables): warp w owns the tile rows
+// 8w .. 8w+7, lane l the columns l, l+32, l+64, l+96 -- the per-row work (y-table decode, row
+// offsets, weights) is shared by 4 pixels, and every store instruction of a warp writes 32
+// consecutive bytes.  Columns at or past the level pitch (the last tile column) are clamped
+// for the loads and not stored.
+struct ColSet {
+    uint32_t x0[4];            // source column of each of the 4 output columns
+    int wa[4], wb[4];          // their x weights 2048 - ax, ax
+    bool ok[4];                // column < pitch
+};
+__device__ __forceinline__ void load_cols(const uint32_t* __restrict__ xt, int tx0, int pitch, ColSet& C)
 {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+    const int lane = (int)(threadIdx.x & 31);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int xo = tx0 + lane + 32 * k;
+        C.ok[k] = xo < pitch;
+        const uint32_t e = __ldg(xt + min(xo, pitch - 1));
+        C.x0[k] = e & 0xFFFFu;
+        C.wb[k] = (int)(e >> 16);
+        C.wa[k] = 2048 - C.wb[k];
+    }
 }
 
-__global__ void __launch_bounds__(kPyrCols) pyramid_staged_kernel(
+// GATHER class, SAFE tables (W, H >= 2: x0 + 1, y0 + 1 always inside): 4 byte gathers per
+// pixel from the frame through L1
+__global__ void __launch_bounds__(kPyrCols) pyramid_gather4_kernel(
     const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
     const LevelInfo* __restrict__ lv, const uint32_t* __restrict__ tiles,
     const uint32_t* __restrict__ tabs)
 {
-    extern __shared__ __align__(16) uint8_t stg[];
     const FrameInfo F = frames[blockIdx.y];
-    if ((int)blockIdx.x >= F.tiles_s) return;
+    if ((int)blockIdx.x >= F.tiles_g) return;
     const uint32_t d = __ldg(tiles + F.tile_off + blockIdx.x);
     const LevelInfo& L = lv[F.level0 + (int)(d & 0xFFu)];
     const int pitch = L.pitch;
     const int tx0 = (int)((d >> 8) & 0xFFu) * kPyrCols;
-    const int ty0 = (int)(d >> 16) * kPyrTileRows;
-    const int nr = min(kPyrTileRows, L.lh - ty0);
+    const int ry = (int)(d >> 16) * kPyrTileRows + 8 * (int)(threadIdx.x >> 5);
+    const int nrw = min(8, L.lh - ry);
+    if (nrw <= 0) return;
     const uint32_t* __restrict__ xt = tabs + L.tab_off;
-    const uint32_t* __restrict__ yt = xt + pitch + ty0;       // padded: 32 entries
-    const int xo = tx0 + (int)threadIdx.x;
-    if (((uintptr_t)F.data | (uintptr_t)F.pitch) & 15u) {      // unaligned rows: byte gathers
-        if (xo >= pitch) return;
-        const uint32_t e = __ldg(xt + xo);
-        const uint8_t* col = F.data + (e & 0xFFFFu);
-        const int ax = (int)(e >> 16);
-        uint8_t* dst = levels + L.offset + xo + (int64_t)ty0 * pitch;
-        for (int r = 0; r < nr; ++r) {
-            const uint32_t ye = __ldg(yt + r);
-            const uint8_t* r0 = col + (int64_t)(ye & 0xFFFFu) * F.pitch;
-            dst[(int64_t)r * pitch] = blend(r0[0], r0[1], r0[F.pitch], r0[F.pitch + 1], ax, (int)(ye >> 16));
-        }
-        return;
-    }
-    // source columns of the tile: from x0 of its first column (rounded down to 16 B) to x0 + 1
-    // of its last (x tables are padded to the pitch, monotone)
-    const int xl = min(tx0 + kPyrCols, pitch) - 1;
-    const int xb = (int)(__ldg(xt + tx0) & 0xFFFFu) & ~15;
-    const int nch = ((int)(__ldg(xt + xl) & 0xFFFFu) + 1 - xb) / 16 + 1;   // <= kStgRS / 16
-    const int RS = nch * 16;
-    // shared row 2r + e = source row y0(ty0 + r) + e: warp w copies rows w, w + 4, ..., lane l
-    // its chunks l, l + 32
+    ColSet C;
+    load_cols(xt, tx0, pitch, C);
+    uint32_t ye[8];
     {
-        const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
-        const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stg);
-        const uint8_t* base = F.data + xb;
-        for (int row = warp; row < 2 * nr; row += kPyrCols / 32) {
-            const int gy = (int)(__ldg(yt + (row >> 1)) & 0xFFFFu) + (row & 1);
-            const uint8_t* src = base + (int64_t)gy * F.pitch;
-            const uint32_t dst = sbase + (uint32_t)(row * RS);
-            for (int c = lane; c < nch; c += 32) cp_async16(dst + 16u * c, src + 16 * c);
-        }
-        asm volatile("cp.async.wait_all;" ::: "memory");
+        const uint4* yt = reinterpret_cast<const uint4*>(xt + pitch + ry);   // padded, aligned
+        const uint4 a = __ldg(yt), b = __ldg(yt + 1);
+        ye[0] = a.x; ye[1] = a.y; ye[2] = a.z; ye[3] = a.w;
+        ye[4] = b.x; ye[5] = b.y; ye[6] = b.z; ye[7] = b.w;
     }
-    __syncthreads();
-    if (xo >= pitch) return;
-    const uint32_t e = __ldg(xt + xo);
-    const int wb = (int)(e >> 16), wa = 2048 - wb;
-    const uint8_t* s = stg + ((int)(e & 0xFFFFu) - xb);
-    uint8_t* dst = levels + L.offset + xo + (int64_t)ty0 * pitch;
-    for (int g0 = 0; g0 < nr; g0 += kPyrRows) {                // CTA-uniform
-        uint32_t ye[kPyrRows];
-        load_rows(yt + g0, ye);
+    const uint32_t fp = (uint32_t)F.pitch;
+    const uint8_t* __restrict__ col[4];
 #pragma unroll
-        for (int r = 0; r < kPyrRows; ++r) {
-            if (g0 + r < nr) {
-                const uint8_t* s0 = s + (2 * (g0 + r)) * RS;
-                const int wd = (int)(ye[r] >> 16), wc = 2048 - wd;
-                const int top = (int)s0[0] * wa + (int)s0[1] * wb;
-                const int bot = (int)s0[RS] * wa + (int)s0[RS + 1] * wb;
-                dst[(int64_t)(g0 + r) * pitch] = (uint8_t)((top * wc + bot * wd + (1 << 21)) >> 22);
+    for (int k = 0; k < 4; ++k) col[k] = F.data + C.x0[k];
+    uint8_t* dst = levels + L.offset + tx0 + (int)(threadIdx.x & 31) + (int64_t)ry * pitch;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        if (r < nrw) {                                          // warp-uniform
+            const uint32_t o = (ye[r] & 0xFFFFu) * fp;
+            const int wd = (int)(ye[r] >> 16), wc = 2048 - wd;
+            int p[4][4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint8_t* q0 = col[k] + o;
+                const uint8_t* q1 = q0 + fp;
+                p[k][0] = __ldg(q0);
+                p[k][1] = __ldg(q0 + 1);
+                p[k][2] = __ldg(q1);
+                p[k][3] = __ldg(q1 + 1);
             }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int top = p[k][0] * C.wa[k] + p[k][1] * C.wb[k];
+                const int bot = p[k][2] * C.wa[k] + p[k][3] * C.wb[k];
+                st_u8_if(dst + 32 * k, (uint32_t)((top * wc + bot * wd + (1 << 21)) >> 22), C.ok[k]);
+            }
+            dst += pitch;
         }
     }
 }
@@ -342,7 +346,7 @@ __global__ void __launch_bounds__(kPyrCols) pyramid_tex_kernel(
 
 }  // namespace
 
-int launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, const int (&max_class)[3],
+int launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, const int (&max_class)[kPyrClasses],
                    bool safe, bool use_tex, uint8_t* levels, const LevelInfo* d_levels,
                    const uint32_t* d_tiles, const uint32_t* d_tabs, cudaStream_t s)
 {
@@ -354,17 +358,10 @@ int launch_pyramid(const FrameInfo* d_frames, int n_frames, int max_tiles, const
     }
     int launched = 0;
     // grid.x = the most tiles any frame has in the class (frames with fewer: surplus CTAs exit)
-    if (max_class[kPyrStaged] > 0) {
-        cudaFuncSetAttribute(pyramid_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kStgSmem);
-        pyramid_staged_kernel<<<dim3(max_class[kPyrStaged], n_frames), kPyrCols, kStgSmem, s>>>(
-            d_frames, levels, d_levels, d_tiles, d_tabs);
-        ++launched;
-    }
     if (max_class[kPyrGather] > 0) {
         const dim3 grid(max_class[kPyrGather], n_frames);
         if (safe)
-            pyramid_kernel<true><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
+            pyramid_gather4_kernel<<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
         else
             pyramid_kernel<false><<<grid, kPyrCols, 0, s>>>(d_frames, levels, d_levels, d_tiles, d_tabs);
         ++launched;

@@ -93,8 +93,8 @@ struct ccnn_ctx {
     int64_t windows_total = 0;
     double s1_mma_flops = 0.0;          // tensor-core FLOPs stage 1 issues for the planned batch
     int pyr_tiles = 0;                  // largest per-frame pyramid tile count
-    int pyr_class_max[3] = {0, 0, 0};   // ... per kernel class (staged, gather, quad)
-    std::vector<int32_t> frame_tiles_s, frame_tiles_g;
+    int pyr_class_max[kPyrClasses] = {};   // ... per kernel class (gather, quad)
+    std::vector<int32_t> frame_tiles_g;
     bool all_safe = true;               // every frame W, H >= 2 (pyramid fast path)
     std::vector<int32_t> frame_level0, frame_nlevels, frame_tiles, frame_tile_off;
     std::vector<uint32_t> ptiles;       // pyramid tile descriptors (pyramid.cu)
@@ -388,7 +388,6 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
     c->frame_tiles.clear();
     c->frame_tile_off.clear();
     c->ptiles.clear();
-    c->frame_tiles_s.clear();
     c->frame_tiles_g.clear();
     c->pyr_tiles = 0;
     for (int& m : c->pyr_class_max) m = 0;
@@ -398,7 +397,7 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
     c->windows_total = 0;
     std::map<std::pair<int, int>, std::vector<int32_t>> tab_cache;   // (W,H) -> tab_off per level
     std::map<std::pair<int, int>, std::pair<int32_t, int32_t>> tile_cache;   // -> (offset, count)
-    std::map<std::pair<int, int>, std::array<int32_t, 3>> class_cache;       // -> count per class
+    std::map<std::pair<int, int>, std::array<int32_t, kPyrClasses>> class_cache;   // -> count per class
     for (int f = 0; f < (int)key.dims.size(); ++f) {
         const int W = key.dims[f].first, H = key.dims[f].second;
         auto it = tab_cache.find(key.dims[f]);
@@ -443,18 +442,17 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
         }
         c->frame_nlevels.push_back(k);
         // pyramid tile descriptors (level-in-frame | tile column << 8 | tile row << 16),
-        // grouped by kernel class (staged | gather | quad), largest levels first within a
+        // grouped by kernel class (gather | quad), largest levels first within a
         // class; shared by equally-sized frames
         if (!have_tabs) {
             tab_cache[key.dims[f]] = new_tabs;
             const int32_t first = (int32_t)c->ptiles.size();
-            int32_t cnt[3] = {0, 0, 0};
+            std::array<int32_t, kPyrClasses> cnt{};
             const bool safe = W >= 2 && H >= 2;
-            for (int cls = 0; cls < 3; ++cls)
+            for (int cls = 0; cls < kPyrClasses; ++cls)
                 for (int l = 0; l < k && l < 256; ++l) {
                     const LevelInfo& L = c->levels[level0 + l];
-                    const int lc = !safe ? kPyrGather : L.sigma >= kPyrQuadSigma ? kPyrQuad
-                                 : L.sigma >= kPyrStagedSigma ? kPyrStaged : kPyrGather;
+                    const int lc = safe && L.sigma >= kPyrQuadSigma ? kPyrQuad : kPyrGather;
                     if (lc != cls) continue;
                     const int tx_n = (L.pitch + kPyrCols - 1) / kPyrCols;
                     const int ty_n = (L.lh + kPyrTileRows - 1) / kPyrTileRows;
@@ -464,16 +462,15 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
                     cnt[cls] += tx_n * ty_n;
                 }
             tile_cache[key.dims[f]] = {first, (int32_t)c->ptiles.size() - first};
-            class_cache[key.dims[f]] = {cnt[0], cnt[1], cnt[2]};
+            class_cache[key.dims[f]] = cnt;
         }
         const auto tc = tile_cache[key.dims[f]];
         const auto cc = class_cache[key.dims[f]];
         c->frame_tile_off.push_back(tc.first);
         c->frame_tiles.push_back(tc.second);
-        c->frame_tiles_s.push_back(cc[0]);
-        c->frame_tiles_g.push_back(cc[1]);
+        c->frame_tiles_g.push_back(cc[kPyrGather]);
         c->pyr_tiles = std::max(c->pyr_tiles, tc.second);
-        for (int cls = 0; cls < 3; ++cls) c->pyr_class_max[cls] = std::max(c->pyr_class_max[cls], cc[cls]);
+        for (int cls = 0; cls < kPyrClasses; ++cls) c->pyr_class_max[cls] = std::max(c->pyr_class_max[cls], cc[cls]);
         c->all_safe = c->all_safe && W >= 2 && H >= 2;
     }
     // slack so that the stage-1 loader's last (clamped) word read stays in bounds
@@ -925,7 +922,6 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
         fi[f].nlevels = ctx->frame_nlevels[f];
         fi[f].tiles = ctx->frame_tiles[f];
         fi[f].tile_off = ctx->frame_tile_off[f];
-        fi[f].tiles_s = ctx->frame_tiles_s[f];
         fi[f].tiles_g = ctx->frame_tiles_g[f];
         fi[f].tex = use_tex ? frame_texture(ctx, fi[f].data, fi[f].w, fi[f].h, fi[f].pitch) : 0;
         use_tex = use_tex && fi[f].tex != 0;
