@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
             auto sync_for_mma = [&]() {
                 tc05::fence_async_smem();
                 tc05::fence_before();
-                __syncthreads();
+                tc05::cta_sync();
             };
             auto wait_l1 = [&]() {
                 tc05::mbar_wait(&bar_l1, ph_l1 & 1); ++ph_l1;
@@ -498,16 +498,16 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 }
                 __syncwarp();
             };
-            __syncthreads();                                   // rows 0..7 in TMEM
+            tc05::cta_sync();                                  // rows 0..7 in TMEM
             tc05::fence_after();
             issue_l1(0);
-            __syncthreads();                                   // rows 8..11, P1 rows 0, 1, D2 zeroed
+            tc05::cta_sync();                                  // rows 8..11, P1 rows 0, 1, D2 zeroed
             tc05::fence_after();
             issue_l1(1);
             issue_l2s(0);
 #pragma unroll 1
             for (int q = 0; q <= NQ + 1; ++q) {
-                __syncthreads();
+                tc05::cta_sync();
                 tc05::fence_after();
                 if (q >= 1 && q <= NQ) issue_l3(q - 1);
                 if (q + 2 <= NQ) issue_l1(q + 2);

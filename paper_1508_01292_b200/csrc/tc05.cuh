@@ -86,6 +86,11 @@ __device__ __forceinline__ uint32_t elect_one()
     return pred;
 }
 
+// CTA barrier 0 for warp-specialised code: the data warps and the MMA warp arrive from
+// different code locations (warp-uniform roles), which the .aligned form behind
+// __syncthreads() does not allow; the non-aligned form counts arrivals only
+__device__ __forceinline__ void cta_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
+
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 // generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
