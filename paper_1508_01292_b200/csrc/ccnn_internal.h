@@ -149,7 +149,8 @@ struct Ctrl {
     uint32_t nms_done;         // NMS last-block ticket
     uint32_t n_out;            // boxes after NMS
     uint32_t nms_overflow;     // a frame exceeded the NMS capacity
-    uint32_t pad[7];
+    uint32_t strip_next;       // selective CNN2 (tcgen05) dynamic strip counter
+    uint32_t pad[6];
 };
 
 constexpr int kMaxLevels = 256;   // pyramid levels per frame (scale_step 1.02 spans 11 octaves)
@@ -185,9 +186,29 @@ int stage1_tc_bmats(const Cnn1W& w, uint16_t* out);   // fills out (kStage1TcBma
 constexpr int kStage1TcBmatHalves = 8 * 96 * 16 + 8 * 96 * 16 + 5 * 24 * 16;   // layers 1, 2, 3
 // selective unit (stage 2/3), persistent over the survivor queue
 struct SelParams { float T2a, T2b; int32_t Tnn, rule; };
-void launch_selective(const Cnn2W& w2, const Cnn3W& w3, SelParams sp, const FrameInfo* d_frames,
-                      const LevelInfo* d_levels, const S1Cand* cands, uint32_t cand_cap, SelOut* out,
-                      float* dbg_resp, AccBox* acc, Ctrl* ctrl, int sm_count, cudaStream_t s);
+// CNN2 on the tensor cores (selective_tc.cu): epilogue constants with Eq. 1's inner factor 2/3
+// folded in (the kernel evaluates Eq. 1 on x' = 2x/3): per layer the accumulator scale
+// (2^-s of the split weights) and biases, layer 4's weights and bias, all x 2/3
+struct Cnn2Tc {
+    float l1s, l1b[16];        // layer 1: b1 - sum_k w1 (O3 folded), scale of w1/127.5 * 2^s
+    float l2s, l2b[6];
+    float l3s, l3b[2];
+    float w4[2], b4;
+};
+int selective_tc_bmats(const Cnn2W& w, uint16_t* out, Cnn2Tc* consts);   // returns the fp16 count
+constexpr int kSelTcBmatHalves = (6 * 128 * 16) + (16 * 96 * 16) + (7 * 32 * 16);
+// stage 2 over strips of kSelTcCands survivors: patch preparation (O5, O2, O6), CNN2 layers
+// 1-3 on tcgen05, layer 4 -> resp2[cand][50] (orientation E then M, 5x5 row-major)
+constexpr int kSelTcCands = 5;
+void launch_selective_cnn2_tc(const Cnn2Tc& k, const uint16_t* d_bmats, const FrameInfo* d_frames,
+                              const LevelInfo* d_levels, const S1Cand* cands, uint32_t cand_cap,
+                              float* resp2, Ctrl* ctrl, int sm_count, cudaStream_t s);
+// stage 3 + the decision per survivor, after launch_selective_cnn2_tc: K2 from resp2; CNN3 (with
+// its own patch preparation) only where the rule needs it (P:99 early stop)
+void launch_selective(const Cnn3W& w3, SelParams sp, const FrameInfo* d_frames,
+                      const LevelInfo* d_levels, const S1Cand* cands, uint32_t cand_cap,
+                      const float* resp2, SelOut* out, float* dbg_resp, AccBox* acc, Ctrl* ctrl,
+                      int sm_count, cudaStream_t s);
 // grouping / NMS per frame + compaction of the results
 void launch_nms(const AccBox* acc, Ctrl* ctrl, int n_frames, int min_cluster, OutBox* staging,
                 int32_t* frame_counts, OutBox* out, cudaStream_t s);

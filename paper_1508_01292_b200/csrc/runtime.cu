@@ -87,6 +87,8 @@ struct ccnn_ctx {
     int s1_grid = 0;
     bool s1_tc = true;                  // stage 1 on tcgen05 (stage1_tc.cu); CCNN_S1_LEGACY=1 -> stage1.cu
     DevBuf s1_bmats;                    // its B matrices
+    DevBuf sel_bmats;                   // selective CNN2 (tcgen05) B matrices
+    Cnn2Tc sel_consts{};                // ... and epilogue constants
     std::vector<uint32_t> tabs;
     int64_t arena_bytes = 0;            // all levels of all frames
     int64_t map_total = 0;              // dense stage-1 map floats (debug)
@@ -114,6 +116,7 @@ struct ccnn_ctx {
         DevBuf ctrl, out;           // control block, compacted boxes
         DevBuf arena;               // all levels of the batch (the pyramid of batch k+1 runs on
                                     // the pyramid stream while batch k's stage 1 reads its own)
+        DevBuf resp2;               // CNN2 responses per survivor (selective_tc.cu)
         DevBuf cands, selout, acc, staging, counts;   // survivor queue .. NMS scratch: the
                                     // selective unit / NMS of batch k (tail stream) overlap
                                     // the stage 1 of batch k+1 (compute stream)
@@ -636,6 +639,12 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
         CU(ctx->s1_bmats.ensure(bm.size() * 2));
         CU(cudaMemcpy(ctx->s1_bmats.p, bm.data(), bm.size() * 2, cudaMemcpyHostToDevice));
     }
+    {
+        std::vector<uint16_t> bm(kSelTcBmatHalves);
+        selective_tc_bmats(ctx->w2, bm.data(), &ctx->sel_consts);
+        CU(ctx->sel_bmats.ensure(bm.size() * 2));
+        CU(cudaMemcpy(ctx->sel_bmats.p, bm.data(), bm.size() * 2, cudaMemcpyHostToDevice));
+    }
     CU(cudaGetLastError());
     for (auto& sl : ctx->slot) {
         CU(cudaMallocHost(&sl.h_ctrl, sizeof(Ctrl)));
@@ -686,7 +695,7 @@ void ccnn_destroy(ccnn_ctx* ctx)
     drop_textures(ctx, nullptr, 0);
     for (DevBuf* b : {&ctx->d_levels, &ctx->d_tasks, &ctx->d_cta_first, &ctx->d_tabs, &ctx->d_ptiles,
                       &ctx->dbg_resp,
-                      &ctx->dbg_map, &ctx->s1_bmats})
+                      &ctx->dbg_map, &ctx->s1_bmats, &ctx->sel_bmats})
         b->release();
     for (auto& sl : ctx->slot) {
         sl.frames.release();
@@ -698,7 +707,7 @@ void ccnn_destroy(ccnn_ctx* ctx)
         sl.ctrl.release();
         sl.out.release();
         sl.arena.release();
-        for (DevBuf* b : {&sl.cands, &sl.selout, &sl.acc, &sl.staging, &sl.counts}) b->release();
+        for (DevBuf* b : {&sl.cands, &sl.selout, &sl.acc, &sl.staging, &sl.counts, &sl.resp2}) b->release();
         if (sl.h_ctrl) cudaFreeHost(sl.h_ctrl);
         for (auto& e : sl.ev) if (e) cudaEventDestroy(e);
         if (sl.ev_user) cudaEventDestroy(sl.ev_user);
@@ -794,6 +803,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     CU(ctx->d_ptiles.ensure(sizeof(uint32_t) * std::max<size_t>(1, ctx->ptiles.size())));
     CU(sl.cands.ensure(sizeof(S1Cand) * cand_cap));
     CU(sl.selout.ensure(sizeof(SelOut) * cand_cap));
+    CU(sl.resp2.ensure(sizeof(float) * 50 * (size_t)cand_cap));
     CU(sl.acc.ensure(sizeof(AccBox) * cand_cap));
     CU(sl.staging.ensure(sizeof(OutBox) * 2 * kNmsCap * (size_t)n));
     CU(sl.counts.ensure(sizeof(int32_t) * n));
@@ -965,8 +975,10 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     cudaStream_t ts = ctx->tail;
     CU(cudaStreamWaitEvent(ts, sl.ev[4], 0));
     CU(cudaEventRecord(sl.ev[8], ts));
-    launch_selective(ctx->w2, ctx->w3, ctx->sp, dfi, ctx->d_levels.as<LevelInfo>(),
-                     sl.cands.as<S1Cand>(), cand_cap, sl.selout.as<SelOut>(),
+    launch_selective_cnn2_tc(ctx->sel_consts, ctx->sel_bmats.as<uint16_t>(), dfi, ctx->d_levels.as<LevelInfo>(),
+                             sl.cands.as<S1Cand>(), cand_cap, sl.resp2.as<float>(), dctrl, ctx->sm_count, ts);
+    launch_selective(ctx->w3, ctx->sp, dfi, ctx->d_levels.as<LevelInfo>(), sl.cands.as<S1Cand>(), cand_cap,
+                     sl.resp2.as<float>(), sl.selout.as<SelOut>(),
                      dbg1 ? ctx->dbg_resp.as<float>() : nullptr, sl.acc.as<AccBox>(), dctrl,
                      ctx->sm_count, ts);
     CU(cudaEventRecord(sl.ev[5], ts));
@@ -1029,7 +1041,7 @@ int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_box
         stats->stage2 = hc.n_stage2;
         stats->stage3 = hc.n_stage3;
         stats->nms = hc.n_out;
-        stats->kernel_launches = 3 + sl.pyr_launches + (sl.n_jobs ? 1 : 0);
+        stats->kernel_launches = 4 + sl.pyr_launches + (sl.n_jobs ? 1 : 0);
         stats->s1_mma_flops = sl.s1_mma_flops;
         const int from[5] = {0, 2, 7, 8, 5}, to[5] = {1, 3, 4, 5, 6};
         for (int k = 0; k < 5; ++k) {

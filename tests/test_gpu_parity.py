@@ -550,8 +550,9 @@ def test_rgb_ingest(ws, cascade):
     got = det.detect_frames(mixed, 20, 1.15)
     assert np.array_equal(got, ref)
     # pyramid (gather and 4-column classes: here min face 20 < 27, so level 0 is upscaled and
-    # both occur), stage 1, selective, NMS, plus one R,G,B -> gray conversion
-    assert det.last_stats["kernel_launches"] == 6
+    # both occur), stage 1, selective CNN2 (tcgen05) and CNN3 + rule, NMS, plus one R,G,B -> gray
+    # conversion
+    assert det.last_stats["kernel_launches"] == 7
     for f in (0, 2):
         for l, (s, lw, lh) in enumerate(oracle.level_table(mixed[f].shape[1], mixed[f].shape[0], 20, 1.15)[:3]):
             assert np.array_equal(det.level_image(f, l), oracle.resample(mixed_gray[f], s, lw, lh))
