@@ -198,16 +198,20 @@ struct Cnn2Tc {
 int selective_tc_bmats(const Cnn2W& w, uint16_t* out, Cnn2Tc* consts);   // returns the fp16 count
 constexpr int kSelTcBmatHalves = (6 * 128 * 16) + (16 * 96 * 16) + (7 * 32 * 16);
 // stage 2 over strips of kSelTcCands survivors: patch preparation (O5, O2, O6), CNN2 layers
-// 1-3 on tcgen05, layer 4 -> resp2[cand][50] (orientation E then M, 5x5 row-major)
+// 1-3 on tcgen05, layer 4 -> resp2[cand][50] (orientation E then M, 5x5 row-major); the
+// equalised patch of every survivor the rule sends to CNN3 -> epatch[cand][kEPatchBytes]
+// (rows of 51 pixels, row-major)
 constexpr int kSelTcCands = 5;
-void launch_selective_cnn2_tc(const Cnn2Tc& k, const uint16_t* d_bmats, const FrameInfo* d_frames,
-                              const LevelInfo* d_levels, const S1Cand* cands, uint32_t cand_cap,
-                              float* resp2, Ctrl* ctrl, int sm_count, cudaStream_t s);
-// stage 3 + the decision per survivor, after launch_selective_cnn2_tc: K2 from resp2; CNN3 (with
-// its own patch preparation) only where the rule needs it (P:99 early stop)
-void launch_selective(const Cnn3W& w3, SelParams sp, const FrameInfo* d_frames,
-                      const LevelInfo* d_levels, const S1Cand* cands, uint32_t cand_cap,
-                      const float* resp2, SelOut* out, float* dbg_resp, AccBox* acc, Ctrl* ctrl,
+constexpr int kEPatchBytes = 2816;             // 55 x 51 = 2805, padded to 16 B
+void launch_selective_cnn2_tc(const Cnn2Tc& k, SelParams sp, const uint16_t* d_bmats,
+                              const FrameInfo* d_frames, const LevelInfo* d_levels,
+                              const S1Cand* cands, uint32_t cand_cap, float* resp2, uint8_t* epatch,
+                              Ctrl* ctrl, int sm_count, cudaStream_t s);
+// stage 3 + the decision per survivor, after launch_selective_cnn2_tc: K2 from resp2; CNN3 on
+// the survivor's equalised patch (epatch) only where the rule needs it (P:99 early stop)
+void launch_selective(const Cnn3W& w3, SelParams sp, const LevelInfo* d_levels,
+                      const S1Cand* cands, uint32_t cand_cap, const float* resp2,
+                      const uint8_t* epatch, SelOut* out, float* dbg_resp, AccBox* acc, Ctrl* ctrl,
                       int sm_count, cudaStream_t s);
 // grouping / NMS per frame + compaction of the results
 void launch_nms(const AccBox* acc, Ctrl* ctrl, int n_frames, int min_cluster, OutBox* staging,

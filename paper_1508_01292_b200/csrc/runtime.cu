@@ -116,7 +116,7 @@ struct ccnn_ctx {
         DevBuf ctrl, out;           // control block, compacted boxes
         DevBuf arena;               // all levels of the batch (the pyramid of batch k+1 runs on
                                     // the pyramid stream while batch k's stage 1 reads its own)
-        DevBuf resp2;               // CNN2 responses per survivor (selective_tc.cu)
+        DevBuf resp2, epatch;       // CNN2 responses / equalised patches per survivor (selective_tc.cu)
         DevBuf cands, selout, acc, staging, counts;   // survivor queue .. NMS scratch: the
                                     // selective unit / NMS of batch k (tail stream) overlap
                                     // the stage 1 of batch k+1 (compute stream)
@@ -707,7 +707,7 @@ void ccnn_destroy(ccnn_ctx* ctx)
         sl.ctrl.release();
         sl.out.release();
         sl.arena.release();
-        for (DevBuf* b : {&sl.cands, &sl.selout, &sl.acc, &sl.staging, &sl.counts, &sl.resp2}) b->release();
+        for (DevBuf* b : {&sl.cands, &sl.selout, &sl.acc, &sl.staging, &sl.counts, &sl.resp2, &sl.epatch}) b->release();
         if (sl.h_ctrl) cudaFreeHost(sl.h_ctrl);
         for (auto& e : sl.ev) if (e) cudaEventDestroy(e);
         if (sl.ev_user) cudaEventDestroy(sl.ev_user);
@@ -804,6 +804,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     CU(sl.cands.ensure(sizeof(S1Cand) * cand_cap));
     CU(sl.selout.ensure(sizeof(SelOut) * cand_cap));
     CU(sl.resp2.ensure(sizeof(float) * 50 * (size_t)cand_cap));
+    CU(sl.epatch.ensure((size_t)kEPatchBytes * cand_cap));
     CU(sl.acc.ensure(sizeof(AccBox) * cand_cap));
     CU(sl.staging.ensure(sizeof(OutBox) * 2 * kNmsCap * (size_t)n));
     CU(sl.counts.ensure(sizeof(int32_t) * n));
@@ -975,10 +976,11 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     cudaStream_t ts = ctx->tail;
     CU(cudaStreamWaitEvent(ts, sl.ev[4], 0));
     CU(cudaEventRecord(sl.ev[8], ts));
-    launch_selective_cnn2_tc(ctx->sel_consts, ctx->sel_bmats.as<uint16_t>(), dfi, ctx->d_levels.as<LevelInfo>(),
-                             sl.cands.as<S1Cand>(), cand_cap, sl.resp2.as<float>(), dctrl, ctx->sm_count, ts);
-    launch_selective(ctx->w3, ctx->sp, dfi, ctx->d_levels.as<LevelInfo>(), sl.cands.as<S1Cand>(), cand_cap,
-                     sl.resp2.as<float>(), sl.selout.as<SelOut>(),
+    launch_selective_cnn2_tc(ctx->sel_consts, ctx->sp, ctx->sel_bmats.as<uint16_t>(), dfi,
+                             ctx->d_levels.as<LevelInfo>(), sl.cands.as<S1Cand>(), cand_cap,
+                             sl.resp2.as<float>(), sl.epatch.as<uint8_t>(), dctrl, ctx->sm_count, ts);
+    launch_selective(ctx->w3, ctx->sp, ctx->d_levels.as<LevelInfo>(), sl.cands.as<S1Cand>(), cand_cap,
+                     sl.resp2.as<float>(), sl.epatch.as<uint8_t>(), sl.selout.as<SelOut>(),
                      dbg1 ? ctx->dbg_resp.as<float>() : nullptr, sl.acc.as<AccBox>(), dctrl,
                      ctx->sm_count, ts);
     CU(cudaEventRecord(sl.ev[5], ts));

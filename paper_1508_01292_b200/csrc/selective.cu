@@ -7,10 +7,10 @@
 // over both orientations, the raw box.
 //
 // B200 design: a persistent kernel drains the survivor queue with a dynamic atomic counter.
-// One CTA per survivor: K2 from resp2 (block count); when CNN3 is needed the CTA rebuilds the
-// equalised patch E (selective_common.cuh, bit-identical to selective_tc.cu's) and runs CNN3 on
-// both orientations on the FFMA pipe (2-map layers: no dense contraction for the tensor
-// cores); only E is stored, the mirrored orientation M(x,y) = E(50-x,y) is read through mirrored
+// One CTA per survivor: K2 from resp2 (block count); when CNN3 is needed the CTA loads the
+// equalised patch E selective_tc.cu left for it and runs CNN3 on both orientations on the FFMA
+// pipe (2-map layers: no dense contraction for the tensor cores); only E is stored, the
+// mirrored orientation M(x,y) = E(50-x,y) is read through mirrored
 // addresses; every layer's work is split over data so the weights a warp uses are warp-uniform
 // constant-bank kernel parameters.
 #include <type_traits>
@@ -39,14 +39,11 @@ __device__ __forceinline__ float act(float x)      // Eq. 1, see stage
 }
 
 struct SelSmem {
-    uint32_t colx[kPatchW], rowy[kPatchH];
-    int hist[256];
-    uint8_t lut[256];
-    uint8_t patch[kPatchN + 3];
     uint32_t eh[kPatchH][kEW];              // E as raw fp16 pixel pairs: word j = pixels (2j, 2j+1),
                                             // pixel 51 = 0 (exact: equalised values <= 255)
     float p2[2][6][12][12];                 // pooled layer 2 [orient][map][y][x]
     float l3[25][2][25];                    // layer-3 activations [map][orient][cell]
+    float w3s[25][3][56];                   // layer-3 weights [map][in][ky*7+kx]; [map][2][0] = bias
     float resp[2][kResp];
     float wmax[kSelThreads / 32];
     int cand;
@@ -63,68 +60,55 @@ __device__ __forceinline__ float img_at(const SelSmem& sm, int y, int x)
     return fmaf(__half2float(h), 1.0f / 127.5f, -1.0f);
 }
 
-// One selective CNN (architecture R: C4x4 1->A, P, C3x3 A->B, P, C7x8 B->C, C1x1 C->1,
-// Eq. 1 after every conv) on both orientations: 51x55 -> 2 x 5x5 responses in sm.resp.
-template <int A, int B, int C>
-__device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
+// CNN3 (architecture R: C4x4 1->2, P, C3x3 2->2, P, C7x8 2->25, C1x1 25->1, Eq. 1 after every
+// conv) on both orientations: 51x55 -> 2 x 5x5 responses in sm.resp.  Work items are register
+// blocked (layer 1: 6 pooled columns per thread, layer 3: one 5-cell response row per thread)
+// so the shared-memory loads per FMA stay low; layer 3's weights are in shared memory (w3s).
+__device__ void run_cnn3(const Cnn3W& W, SelSmem& sm, float* p1)
 {
     const int tid = threadIdx.x;
-    // layers 1-2 in chunks of AC input maps: P1 holds one chunk (both orientations), layer 2
-    // accumulates over the chunks in registers
-    constexpr int AC = A;
-    constexpr int NCH = A / AC;
-    const bool l2_item = tid < 2 * 132;
-    const int o2 = tid / 132, pos2 = tid - o2 * 132, py2 = pos2 / 11, px2 = pos2 - py2 * 11;
-    static_assert(B % 2 == 0, "layer 2 runs on map pairs");
-    float2 s2[B / 2][4];                           // (map 2 bp, map 2 bp + 1) x pool position
+    // ---- layer 1: conv4x4 1->2, pool, act; item = (orientation, pooled row, 6 pooled columns)
+    for (int it = tid; it < 2 * 26 * 4; it += kSelThreads) {
+        const int o = it / 104, rem = it - o * 104, py0 = rem >> 2, g = rem & 3;
+        float x[5][15];                             // image rows 2py0 .. +4, columns 12g .. +14
 #pragma unroll
-    for (int bp = 0; bp < B / 2; ++bp)
+        for (int r = 0; r < 5; ++r)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) s2[bp][k] = make_float2(W.b2[2 * bp], W.b2[2 * bp + 1]);
-#pragma unroll 1
-    for (int ch = 0; ch < NCH; ++ch) {
-    // ---- layer 1: conv4x4 1->A, pool, act; item = (orientation, pooled pos), all A maps ----
-    for (int it = tid; it < 1248; it += kSelThreads) {
-        // a warp's lanes span two pooled rows (2 image rows apart); the mirrored orientation
-        // walks its row backwards so its image words also increase with the lane
-        const int o = it / 624, rem = it - o * 624, py0 = rem / 24;
-        const int px0 = (o == 0) ? rem - py0 * 24 : 23 - (rem - py0 * 24);
-        float x[5][5];
-        if (o == 0) {
+            for (int c = 0; c < 15; ++c)            // M(x, y) = E(50 - x, y); column 51+ unused
+                x[r][c] = img_at(sm, 2 * py0 + r, o == 0 ? min(12 * g + c, 50) : max(50 - 12 * g - c, 0));
 #pragma unroll
-            for (int r = 0; r < 5; ++r)
-#pragma unroll
-                for (int c = 0; c < 5; ++c) x[r][c] = img_at(sm, 2 * py0 + r, 2 * px0 + c);
-        } else {                                    // M(x, y) = E(50 - x, y)
-#pragma unroll
-            for (int r = 0; r < 5; ++r)
-#pragma unroll
-                for (int c = 0; c < 5; ++c) x[r][c] = img_at(sm, 2 * py0 + r, 50 - 2 * px0 - c);
-        }
-#pragma unroll
-        for (int a = 0; a < A; ++a) {
-            float sv[4];
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                sv[p] = W.b1[a];
-#pragma unroll
-                for (int ky = 0; ky < 4; ++ky)
-#pragma unroll
-                    for (int kx = 0; kx < 4; ++kx)
-                        sv[p] = fmaf(W.w1[a][ky * 4 + kx], x[(p >> 1) + ky][(p & 1) + kx], sv[p]);
-            }
+        for (int j = 0; j < 6; ++j) {               // pooled column px0 = 6g + j
+            const int px0 = 6 * g + j;
             const int col = (px0 & 1) ? kP1Odd + (px0 >> 1) : (px0 >> 1);
-            p1[(o * AC + a) * kP1MS + py0 * kP1RS + col] =
-                act(fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3])));   // pool then act
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                float sv[4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    sv[p] = W.b1[a];
+#pragma unroll
+                    for (int ky = 0; ky < 4; ++ky)
+#pragma unroll
+                        for (int kx = 0; kx < 4; ++kx)
+                            sv[p] = fmaf(W.w1[a][ky * 4 + kx], x[(p >> 1) + ky][2 * j + (p & 1) + kx], sv[p]);
+                }
+                p1[(o * 2 + a) * kP1MS + py0 * kP1RS + col] =
+                    act(fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3])));   // pool then act
+            }
         }
     }
     __syncthreads();
-    // ---- layer 2 (partial over this chunk's maps): conv3x3 A->B; item = (orientation,
-    //      pooled position), all output maps ----
-    if (l2_item) {
-#pragma unroll 1
-        for (int a = 0; a < AC; ++a) {              // uniform counter: LDCU [UR+imm]
-            const float* in = p1 + (o2 * AC + a) * kP1MS + 2 * py2 * kP1RS;
+    // ---- layer 2: conv3x3 2->2, pool, act; item = (orientation, pooled position) ----
+    if (tid < 2 * 132) {
+        const int o2 = tid / 132, pos2 = tid - o2 * 132, py2 = pos2 / 11, px2 = pos2 - py2 * 11;
+        float s2[2][4];
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s2[b][k] = W.b2[b];
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            const float* in = p1 + (o2 * 2 + a) * kP1MS + 2 * py2 * kP1RS;
             float v[4][4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
@@ -133,97 +117,63 @@ __device__ void run_net(const SelNetW<A, B, C>& W, SelSmem& sm, float* p1)
                 v[r][2] = in[r * kP1RS + px2 + 1];
                 v[r][3] = in[r * kP1RS + kP1Odd + px2 + 1];
             }
-            constexpr int NV = SelNetW<A, B, C>::W2V;
-            float wv[NV];
-            const float4* w4p = reinterpret_cast<const float4*>(W.w2v[ch * AC + a]);
 #pragma unroll
-            for (int k4 = 0; k4 < NV / 4; ++k4) {
-                const float4 t4 = w4p[k4];
-                wv[4 * k4] = t4.x; wv[4 * k4 + 1] = t4.y; wv[4 * k4 + 2] = t4.z; wv[4 * k4 + 3] = t4.w;
-            }
-#pragma unroll
-            for (int bp = 0; bp < B / 2; ++bp)
+            for (int b = 0; b < 2; ++b)
 #pragma unroll
                 for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
-                    for (int kx = 0; kx < 3; ++kx) {
-                        const float2 w = make_float2(wv[(ky * 3 + kx) * B + 2 * bp], wv[(ky * 3 + kx) * B + 2 * bp + 1]);
+                    for (int kx = 0; kx < 3; ++kx)
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const float x = v[(k >> 1) + ky][(k & 1) + kx];
-                            s2[bp][k] = __ffma2_rn(w, make_float2(x, x), s2[bp][k]);
-                        }
-                    }
+                        for (int k = 0; k < 4; ++k)
+                            s2[b][k] = fmaf(W.w2[b][a][ky * 3 + kx], v[(k >> 1) + ky][(k & 1) + kx], s2[b][k]);
         }
-    }
-    if (ch + 1 < NCH) __syncthreads();             // the next chunk overwrites P1
-    }
-    if (l2_item) {
 #pragma unroll
-        for (int bp = 0; bp < B / 2; ++bp) {
-            sm.p2[o2][2 * bp][py2][px2] =
-                act(fmaxf(fmaxf(s2[bp][0].x, s2[bp][1].x), fmaxf(s2[bp][2].x, s2[bp][3].x)));
-            sm.p2[o2][2 * bp + 1][py2][px2] =
-                act(fmaxf(fmaxf(s2[bp][0].y, s2[bp][1].y), fmaxf(s2[bp][2].y, s2[bp][3].y)));
-        }
+        for (int b = 0; b < 2; ++b)
+            sm.p2[o2][b][py2][px2] = act(fmaxf(fmaxf(s2[b][0], s2[b][1]), fmaxf(s2[b][2], s2[b][3])));
     }
     __syncthreads();
-    // ---- layer 3: conv7x8 B->C, act; item = (map, orientation, cell) ----
-    if constexpr (C == 2) {
-        if (tid < 128) {                            // map = warp pair -> warp-uniform weights
-            const int m = tid >> 6, idx = tid & 63;
-            if (idx < 50) {
-                const int o = idx / 25, cell = idx - o * 25, y = cell / 5, x = cell - y * 5;
-                auto body = [&](auto Mc) {
-                    constexpr int M = decltype(Mc)::value;
-                    float s = W.b3[M];
+    // ---- layer 3: conv7x8 2->25, act; item = (map, orientation, response row): 250 items ----
+    if (tid < 250) {
+        const int m = tid / 10, o = (tid / 5) & 1, y = tid % 5;
+        float acc[5];
 #pragma unroll
-                    for (int b = 0; b < B; ++b)
+        for (int xx = 0; xx < 5; ++xx) acc[xx] = sm.w3s[m][2][0];   // bias
+#pragma unroll 1
+        for (int ch = 0; ch < 2; ++ch) {
+#pragma unroll 2
+            for (int ky = 0; ky < 8; ++ky) {
+                const float* row = &sm.p2[o][ch][y + ky][0];
+                float v[11];
 #pragma unroll
-                        for (int ky = 0; ky < 8; ++ky)
+                for (int c = 0; c < 11; ++c) v[c] = row[c];
+                const float* wr = &sm.w3s[m][ch][ky * 7];
 #pragma unroll
-                            for (int kx = 0; kx < 7; ++kx)
-                                s = fmaf(W.w3[M][b][ky * 7 + kx], sm.p2[o][b][y + ky][x + kx], s);
-                    sm.l3[M][o][cell] = act(s);
-                };
-                if (m == 0) body(std::integral_constant<int, 0>{});
-                else body(std::integral_constant<int, 1>{});
+                for (int kx = 0; kx < 7; ++kx) {
+                    const float w = wr[kx];
+#pragma unroll
+                    for (int xx = 0; xx < 5; ++xx) acc[xx] = fmaf(w, v[xx + kx], acc[xx]);
+                }
             }
         }
-    } else {
-        // map-major items padded to 64 per map: every warp works on one map, so its weight
-        // loads are one broadcast address (no serialised constant-cache accesses)
-        for (int it = tid; it < C * 64; it += kSelThreads) {
-            const int m = it >> 6, idx = it & 63;
-            if (idx >= 50) continue;
-            const int o = idx / 25, cell = idx - o * 25, y = cell / 5, x = cell - y * 5;
-            float s = W.b3[m];
 #pragma unroll
-            for (int b = 0; b < B; ++b)
-#pragma unroll
-                for (int ky = 0; ky < 8; ++ky)
-#pragma unroll
-                    for (int kx = 0; kx < 7; ++kx)
-                        s = fmaf(W.w3[m][b][ky * 7 + kx], sm.p2[o][b][y + ky][x + kx], s);
-            sm.l3[m][o][cell] = act(s);
-        }
+        for (int xx = 0; xx < 5; ++xx) sm.l3[m][o][y * 5 + xx] = act(acc[xx]);
     }
     __syncthreads();
-    // ---- layer 4: C1x1 C->1, act ----
+    // ---- layer 4: C1x1 25->1, act ----
     if (tid < 2 * kResp) {
         const int o = tid / kResp, cell = tid - o * kResp;
         float r = W.b4;
 #pragma unroll
-        for (int c = 0; c < C; ++c) r = fmaf(W.w4[c], sm.l3[c][o][cell], r);
+        for (int c = 0; c < 25; ++c) r = fmaf(W.w4[c], sm.l3[c][o][cell], r);
         sm.resp[o][cell] = act(r);
     }
     __syncthreads();
 }
 
 __global__ void __launch_bounds__(kSelThreads, 3) selective_kernel(
-    const __grid_constant__ Cnn3W W3, const SelParams sp, const FrameInfo* __restrict__ frames,
-    const LevelInfo* __restrict__ lvinfo, const S1Cand* __restrict__ cands, const uint32_t cand_cap,
-    const float* __restrict__ resp2, SelOut* __restrict__ out, float* __restrict__ dbg_resp,
+    const __grid_constant__ Cnn3W W3, const SelParams sp, const LevelInfo* __restrict__ lvinfo,
+    const S1Cand* __restrict__ cands, const uint32_t cand_cap, const float* __restrict__ resp2,
+    const uint8_t* __restrict__ epatch, SelOut* __restrict__ out, float* __restrict__ dbg_resp,
     AccBox* __restrict__ acc, Ctrl* __restrict__ ctrl)
 {
     extern __shared__ __align__(16) unsigned char sraw[];
@@ -245,6 +195,10 @@ __global__ void __launch_bounds__(kSelThreads, 3) selective_kernel(
         return r;
     };
 
+    for (int i = tid; i < 25 * 3 * 56; i += kSelThreads) {
+        const int m = i / 168, r = i - m * 168, ch = r / 56, k = r - ch * 56;
+        sm.w3s[m][ch][k] = ch < 2 ? W3.w3[m][ch][k] : (k == 0 ? W3.b3[m] : 0.f);
+    }
     for (;;) {
         if (tid == 0) sm.cand = (int)atomicAdd(&ctrl->sel_next, 1u);
         __syncthreads();
@@ -263,42 +217,19 @@ __global__ void __launch_bounds__(kSelThreads, 3) selective_kernel(
             delta = (sp.rule == 0) ? 0 : 1;
             best = block_max(r2v);
         } else {
-            const FrameInfo F = frames[lvinfo[cd.level].frame];
-            // ---- the equalised patch E (O5, O2, O6; selective_common.cuh) ----
-            if (tid < kPatchW) sm.colx[tid] = sel::patch_col(cd.ix, sigma, tid, F.w);
-            else if (tid < kPatchW + kPatchH) sm.rowy[tid - kPatchW] = sel::patch_row(cd.iy, sigma, tid - kPatchW, F.h);
-            if (tid < 256) sm.hist[tid] = 0;
-            __syncthreads();
-            for (int k0 = tid; k0 < kPatchN; k0 += 4 * kSelThreads) {
-                uint32_t val[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int k = min(k0 + u * kSelThreads, kPatchN - 1);
-                    const int v = k / kPatchW, uu = k - v * kPatchW;
-                    val[u] = sel::sample(F.data, F.pitch, F.w, F.h, sm.colx[uu], sm.rowy[v]);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int k = k0 + u * kSelThreads;
-                    if (k >= kPatchN) break;
-                    sm.patch[k] = (uint8_t)val[u];
-                    atomicAdd(&sm.hist[val[u]], 1);
-                }
-            }
-            __syncthreads();
-            if (tid < 32) sel::warp_lut(sm.hist, sm.lut);
-            __syncthreads();
-            // E as fp16 pixel pairs (raw equalised values; O3 is applied by the layers)
+            // ---- the equalised patch E (selective_tc.cu wrote it for every survivor the rule
+            //      sends here) as fp16 pixel pairs (raw values; O3 is applied by the layers) ----
+            const uint8_t* ep = epatch + (int64_t)ci * kEPatchBytes;
             for (int k = tid; k < kPatchH * 26; k += kSelThreads) {
                 const int v = k / 26, j = k - v * 26;
-                const uint32_t p0 = sm.lut[sm.patch[v * kPatchW + 2 * j]];
-                const uint32_t p1v = (2 * j + 1 < kPatchW) ? sm.lut[sm.patch[v * kPatchW + 2 * j + 1]] : 0u;
+                const uint32_t p0 = __ldg(ep + v * kPatchW + 2 * j);
+                const uint32_t p1v = (2 * j + 1 < kPatchW) ? __ldg(ep + v * kPatchW + 2 * j + 1) : 0u;
                 const __half2 h = __floats2half2_rn((float)p0, (float)p1v);
                 sm.eh[v][j] = *reinterpret_cast<const uint32_t*>(&h);
             }
             __syncthreads();
             // ---- CNN3 on both orientations, K3, the rule (P:95 / P:217) ----
-            run_net<2, 2, 25>(W3, sm, p1);
+            run_cnn3(W3, sm, p1);
             if (tid < 2 * kResp) r3v = sm.resp[tid / kResp][tid % kResp];
             K3 = __syncthreads_count(tid < 2 * kResp && r3v > sp.T2b);
             ran3 = 1;
@@ -335,9 +266,9 @@ size_t selective_smem_bytes()
     return ((sizeof(SelSmem) + 15) & ~size_t(15)) + sizeof(float) * kP1Floats;
 }
 
-void launch_selective(const Cnn3W& w3, SelParams sp, const FrameInfo* d_frames,
-                      const LevelInfo* d_levels, const S1Cand* cands, uint32_t cand_cap,
-                      const float* resp2, SelOut* out, float* dbg_resp, AccBox* acc, Ctrl* ctrl,
+void launch_selective(const Cnn3W& w3, SelParams sp, const LevelInfo* d_levels,
+                      const S1Cand* cands, uint32_t cand_cap, const float* resp2,
+                      const uint8_t* epatch, SelOut* out, float* dbg_resp, AccBox* acc, Ctrl* ctrl,
                       int sm_count, cudaStream_t s)
 {
     const size_t smem = selective_smem_bytes();
@@ -345,8 +276,8 @@ void launch_selective(const Cnn3W& w3, SelParams sp, const FrameInfo* d_frames,
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, selective_kernel, kSelThreads, smem);
     if (occ < 1) occ = 1;
-    selective_kernel<<<sm_count * occ, kSelThreads, smem, s>>>(w3, sp, d_frames, d_levels, cands, cand_cap,
-                                                              resp2, out, dbg_resp, acc, ctrl);
+    selective_kernel<<<sm_count * occ, kSelThreads, smem, s>>>(w3, sp, d_levels, cands, cand_cap, resp2,
+                                                              epatch, out, dbg_resp, acc, ctrl);
 }
 
 }  // namespace ccnn

@@ -25,23 +25,38 @@ __device__ __forceinline__ uint32_t bilin_coord(double s, int n)
     return (uint32_t)(int)f | ((uint32_t)a << 16);
 }
 
-// O5: sampling coordinate of patch column u (0..50) / row v (0..54) of the survivor (ix, iy)
-// of a level with scale sigma, as an O2 table entry i0 | a << 16
+// O5: the patch region of the survivor (ix, iy) of a level with scale sigma: left edge rx and
+// width rw (columns), top edge ry and height rh (rows), in original-image pixels
+struct PatchRegion { double rx, rw, ry, rh; };
+__device__ __forceinline__ PatchRegion patch_region(int ix, int iy, double sigma)
+{
+    PatchRegion g;
+    const double cx = __ddiv_rn(__dadd_rn((double)(4 * ix), 13.5), sigma);
+    const double cy = __ddiv_rn(__dadd_rn((double)(4 * iy), 15.5), sigma);
+    g.rw = __ddiv_rn(__ddiv_rn(1377.0, 35.0), sigma);            // 27*51/35
+    g.rh = __ddiv_rn(__ddiv_rn(1705.0, 39.0), sigma);            // 31*55/39
+    g.rx = __dsub_rn(cx, __ddiv_rn(g.rw, 2.0));
+    g.ry = __dsub_rn(cy, __ddiv_rn(g.rh, 2.0));
+    return g;
+}
+// sampling coordinate of patch column u (0..50) / row v (0..54) as an O2 table entry
+__device__ __forceinline__ uint32_t region_col(const PatchRegion& g, int u, int W)
+{
+    const double t = __ddiv_rn(__dmul_rn(__dadd_rn((double)u, 0.5), g.rw), 51.0);
+    return bilin_coord(__dsub_rn(__dadd_rn(g.rx, t), 0.5), W);
+}
+__device__ __forceinline__ uint32_t region_row(const PatchRegion& g, int v, int H)
+{
+    const double t = __ddiv_rn(__dmul_rn(__dadd_rn((double)v, 0.5), g.rh), 55.0);
+    return bilin_coord(__dsub_rn(__dadd_rn(g.ry, t), 0.5), H);
+}
 __device__ __forceinline__ uint32_t patch_col(int ix, double sigma, int u, int W)
 {
-    const double cx = __ddiv_rn(__dadd_rn((double)(4 * ix), 13.5), sigma);
-    const double rw = __ddiv_rn(__ddiv_rn(1377.0, 35.0), sigma);   // 27*51/35
-    const double rx = __dsub_rn(cx, __ddiv_rn(rw, 2.0));
-    const double t = __ddiv_rn(__dmul_rn(__dadd_rn((double)u, 0.5), rw), 51.0);
-    return bilin_coord(__dsub_rn(__dadd_rn(rx, t), 0.5), W);
+    return region_col(patch_region(ix, 0, sigma), u, W);
 }
 __device__ __forceinline__ uint32_t patch_row(int iy, double sigma, int v, int H)
 {
-    const double cy = __ddiv_rn(__dadd_rn((double)(4 * iy), 15.5), sigma);
-    const double rh = __ddiv_rn(__ddiv_rn(1705.0, 39.0), sigma);   // 31*55/39
-    const double ry = __dsub_rn(cy, __ddiv_rn(rh, 2.0));
-    const double t = __ddiv_rn(__dmul_rn(__dadd_rn((double)v, 0.5), rh), 55.0);
-    return bilin_coord(__dsub_rn(__dadd_rn(ry, t), 0.5), H);
+    return region_row(patch_region(0, iy, sigma), v, H);
 }
 
 // O2 blend of the 2x2 footprint at table entries xt (column) / yt (row) of a frame

@@ -45,8 +45,11 @@
 namespace ccnn {
 namespace {
 
-constexpr int NDW = 8;                         // data warps
-constexpr int NT = 32 * (NDW + 1);             // + the MMA warp
+constexpr int NDW = 8;                         // data warps 0..7
+constexpr int NPW = 8;                         // patch-preparation warps 9..16
+constexpr int NPIPE = 32 * (NDW + 1);          // pipeline threads: data warps + the MMA warp (8)
+constexpr int NT = NPIPE + 32 * NPW;           // + the preparation warps
+constexpr uint32_t BAR_PIPE = 1, BAR_PREP = 2; // named barriers of the two groups
 constexpr int NC = kSelTcCands;                // survivors per strip: 2 NC patch slots
 constexpr int SL = 12;                         // TMEM lanes per patch slot (P2 columns 0..11)
 constexpr int NQ = 12;                         // P2 rows of a patch (0..11)
@@ -70,17 +73,21 @@ constexpr int P1_RING = 4;                     // P1 rows 2u .. 2u+3 live
 constexpr int P2_E = 136;                      // P2 entries per (buffer, part): 128 written + reach
 constexpr int P2_HL = P2_E * 16;
 constexpr int P2_BUF = 2 * P2_HL;
-struct Prep {                                  // per preparing warp
-    uint32_t colx[64], rowy[64];
+struct Prep {                                  // per survivor of the strip being prepared
+    uint32_t colx[64], rowy[64];               // O2 table entries of the patch columns / rows
     int hist[256];
     uint8_t lut[256];
+    const uint8_t* data;                       // its frame
+    int64_t pitch;
+    int32_t w, h;
+    sel::PatchRegion g;                        // O5 region
 };
 constexpr int OFF_B1 = 0, OFF_B2 = OFF_B1 + B1_BYTES, OFF_B3 = OFF_B2 + B2_BYTES;
 constexpr int OFF_P1 = OFF_B3 + B3_BYTES;
 constexpr int OFF_P2 = OFF_P1 + P1_RING * P1_SLOT;
-constexpr int OFF_E = OFF_P2 + 2 * P2_BUF;
-constexpr int OFF_PREP = OFF_E + NC * PATCH_BYTES;
-constexpr int SMEM_BYTES = OFF_PREP + NC * (int)sizeof(Prep);
+constexpr int OFF_E = OFF_P2 + 2 * P2_BUF;    // two strips of patches (double buffer)
+constexpr int OFF_PREP = OFF_E + 2 * NC * PATCH_BYTES;
+constexpr int SMEM_BYTES = OFF_PREP + 2 * NC * (int)sizeof(Prep);   // geometry one strip ahead
 static_assert(OFF_E % 16 == 0 && OFF_PREP % 16 == 0, "alignment");
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 // TMEM columns (512 allocated: one CTA per SM)
@@ -159,63 +166,107 @@ __device__ __forceinline__ void st_zero24(uint32_t taddr)
         :: "r"(taddr), "r"(taddr + 16u), "r"(0u) : "memory");
 }
 
-// patch preparation of survivor `cd` by one warp into the 56 x 64-B rows at `ep`
-__device__ __forceinline__ void prep_patch(const S1Cand& cd, const LevelInfo* __restrict__ lvinfo,
-                                           const FrameInfo* __restrict__ frames, uint8_t* ep, Prep& P)
+// patch preparation of the nc survivors c0 .. c0+nc-1 of a strip by the 128 threads of the
+// preparation warps, in two parts: prep_geometry (O5 sampling tables of every patch column /
+// row; run one strip ahead, while the previous strip's sampling is still to come) and prep_sample (O2
+// sampling into the 56 x 64-B patch rows at ebuf -- pixel x of row y at byte y*64 + 4 + x --,
+// histogram, O6 LUT; the data warps equalise the pixels as they load them)
+__device__ __forceinline__ void prep_geometry(int c0, int nc, const S1Cand* __restrict__ cands,
+                                              const LevelInfo* __restrict__ lvinfo,
+                                              const FrameInfo* __restrict__ frames, Prep* P)
 {
-    const int lane = (int)(threadIdx.x & 31);
-    const LevelInfo& L = lvinfo[cd.level];
-    const double sigma = L.sigma;
-    const FrameInfo F = frames[L.frame];
-    for (int u = lane; u < kPatchW; u += 32) P.colx[u] = sel::patch_col(cd.ix, sigma, u, F.w);
-    for (int v = lane; v < kPatchH; v += 32) P.rowy[v] = sel::patch_row(cd.iy, sigma, v, F.h);
-    for (int k = lane; k < 256; k += 32) P.hist[k] = 0;
-    for (int k = lane; k < PATCH_BYTES / 16; k += 32) reinterpret_cast<uint4*>(ep)[k] = make_uint4(0, 0, 0, 0);
-    __syncwarp();
-    // O2 sampling, 4 pixels per lane per pass so their gathers are in flight together
-    for (int k0 = lane; k0 < kPatchN; k0 += 128) {
-        uint32_t val[4];
-        int off[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int k = min(k0 + 32 * q, kPatchN - 1);
-            const int v = k / kPatchW, u = k - v * kPatchW;
-            val[q] = sel::sample(F.data, F.pitch, F.w, F.h, P.colx[u], P.rowy[v]);
-            off[q] = v * EP + 4 + u;
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (k0 + 32 * q < kPatchN) {
-                ep[off[q]] = (uint8_t)val[q];
-                atomicAdd(&P.hist[val[q]], 1);
-            }
-        }
+    const int pt = (int)threadIdx.x - NPIPE;                  // 0 .. 32 NPW - 1
+    if (pt < nc) {                                             // per survivor: region, frame
+        const S1Cand cd = cands[c0 + pt];
+        const LevelInfo& L = lvinfo[cd.level];
+        const FrameInfo& F = frames[L.frame];
+        Prep& Q = P[pt];
+        Q.g = sel::patch_region(cd.ix, cd.iy, L.sigma);
+        Q.data = F.data; Q.pitch = F.pitch; Q.w = F.w; Q.h = F.h;
     }
-    __syncwarp();
-    sel::warp_lut(P.hist, P.lut);
-    __syncwarp();
-    for (int k = lane; k < kPatchN; k += 32) {                // equalise in place (O6)
-        const int v = k / kPatchW, u = k - v * kPatchW;
-        uint8_t* p = ep + v * EP + 4 + u;
-        *p = P.lut[*p];
+    tc05::named_sync(BAR_PREP, 32 * NPW);
+    for (int i = pt; i < nc * (kPatchW + kPatchH); i += 32 * NPW) {
+        const int c = i / (kPatchW + kPatchH), j = i - c * (kPatchW + kPatchH);
+        Prep& Q = P[c];
+        if (j < kPatchW) Q.colx[j] = sel::region_col(Q.g, j, Q.w);
+        else Q.rowy[j - kPatchW] = sel::region_row(Q.g, j - kPatchW, Q.h);
     }
 }
 
+__device__ __forceinline__ void prep_sample(int nc, uint8_t* ebuf, Prep* P)
+{
+    const int pt = (int)threadIdx.x - NPIPE;                  // 0 .. 32 NPW - 1
+    auto psync = [] { tc05::named_sync(BAR_PREP, 32 * NPW); };
+    for (int i = pt; i < nc * 256; i += 32 * NPW) P[i >> 8].hist[i & 255] = 0;
+    psync();
+    // O2 sampling: thread = patch column u (pt & 63; 51 active) x row phase (pt >> 6) over the
+    // strip's nc x 55 patch rows, 8 rows per pass so 32 byte gathers are in flight per thread
+    // (the frames are in HBM: latency-bound otherwise)
+    constexpr int RP = 32 * NPW / 64;                          // row phases
+    const int u = pt & 63, rs = pt >> 6;
+    const int nrows = nc * kPatchH;
+    constexpr int RU = 4;
+    for (int r0 = rs; r0 < nrows; r0 += RP * RU) {
+        uint32_t px[RU][4], axy[RU];
+        int off[RU], cc[RU];
+#pragma unroll
+        for (int j = 0; j < RU; ++j) {
+            const int r = min(r0 + RP * j, nrows - 1);
+            const int c = r / kPatchH, v = r - c * kPatchH;
+            const Prep& Q = P[c];
+            const uint32_t xt = Q.colx[min(u, kPatchW - 1)], yt = Q.rowy[v];
+            const uint32_t x0 = xt & 0xFFFFu, y0 = yt & 0xFFFFu;
+            const uint32_t x1 = min(x0 + 1u, (uint32_t)(Q.w - 1)), y1 = min(y0 + 1u, (uint32_t)(Q.h - 1));
+            const uint8_t* q0 = Q.data + (int64_t)y0 * Q.pitch;
+            const uint8_t* q1 = Q.data + (int64_t)y1 * Q.pitch;
+#ifndef SELTC_NO_LOAD                                           // timing experiments only
+            px[j][0] = __ldg(q0 + x0);
+            px[j][1] = __ldg(q0 + x1);
+            px[j][2] = __ldg(q1 + x0);
+            px[j][3] = __ldg(q1 + x1);
+#else
+            px[j][0] = (uint32_t)(uintptr_t)q0 & 255u; px[j][1] = x1 & 255u; px[j][2] = y1 & 255u;
+            px[j][3] = (uint32_t)(uintptr_t)q1 & 255u;
+#endif
+            axy[j] = (xt >> 16) | (yt & 0xFFFF0000u);
+            off[j] = c * PATCH_BYTES + v * EP + 4 + u;
+            cc[j] = c;
+        }
+#pragma unroll
+        for (int j = 0; j < RU; ++j) {
+            if (u < kPatchW && r0 + RP * j < nrows) {
+                const uint32_t ax = axy[j] & 0xFFFFu, ay = axy[j] >> 16;
+                const uint32_t top = px[j][0] * (2048u - ax) + px[j][1] * ax;
+                const uint32_t bot = px[j][2] * (2048u - ax) + px[j][3] * ax;
+                const uint32_t val = (top * (2048u - ay) + bot * ay + (1u << 21)) >> 22;
+                ebuf[off[j]] = (uint8_t)val;
+#ifndef SELTC_NO_HIST                                           // timing experiments only
+                atomicAdd(&P[cc[j]].hist[val], 1);
+#endif
+            }
+        }
+    }
+    psync();
+    for (int c = pt >> 5; c < nc; c += NPW) sel::warp_lut(P[c].hist, P[c].lut);
+    psync();
+}
+
 __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
-    const __grid_constant__ Cnn2Tc K, const uint16_t* __restrict__ bmats,
+    const __grid_constant__ Cnn2Tc K, const SelParams sp, const uint16_t* __restrict__ bmats,
     const FrameInfo* __restrict__ frames, const LevelInfo* __restrict__ lvinfo,
     const S1Cand* __restrict__ cands, const uint32_t cand_cap, float* __restrict__ resp2,
-    Ctrl* __restrict__ ctrl)
+    uint8_t* __restrict__ epatch, Ctrl* __restrict__ ctrl)
 {
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ int s_strip;
+    __shared__ int s_claim, s_strip[2], s_nc[2], s_k2[2][NC];
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) uint64_t bar_l1, bar_l2, bar_l3;
+    __shared__ __align__(8) uint64_t bar_l1, bar_l2, bar_l3, bar_full[2], bar_empty[2];
 
     const int tid = threadIdx.x;
     const int warp = __shfl_sync(0xFFFFFFFFu, tid >> 5, 0);   // provably warp-uniform
     const int lane = tid & 31;
     const bool mma_warp = warp == NDW;
+    const bool prep_warp = warp > NDW;
     const int n_cand = (int)min(*(volatile uint32_t*)&ctrl->n_cand, cand_cap);
     const int n_strips = (n_cand + NC - 1) / NC;
     if ((int)blockIdx.x >= n_strips) return;                   // CTA-uniform, before any barrier
@@ -233,6 +284,10 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
         tc05::mbar_init(&bar_l1, 1);
         tc05::mbar_init(&bar_l2, 1);
         tc05::mbar_init(&bar_l3, 1);
+        for (int b = 0; b < 2; ++b) {
+            tc05::mbar_init(&bar_full[b], 32 * NPW);           // every preparation thread
+            tc05::mbar_init(&bar_empty[b], NDW);               // one thread per data warp
+        }
         tc05::mbar_fence_init();
     }
     tc05::fence_async_smem();
@@ -248,38 +303,85 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
     const uint32_t t_lane = (uint32_t)(32 * qd) << 16;
     const int slot = m / SL, xp = m - slot * SL;   // patch slot, P2 column within the patch
 
-    for (;;) {
-        if (tid == 0) s_strip = (int)atomicAdd(&ctrl->strip_next, 1u);
-        __syncthreads();
-        const int st = s_strip;
-        if (st >= n_strips) break;
-        const int c0 = st * NC;
-        const int nc = min(NC, n_cand - c0);
-        // ---- patch preparation: warp w < nc prepares survivor c0 + w ----
-        if (warp < nc) {
-            const S1Cand cd = cands[c0 + warp];
-            prep_patch(cd, lvinfo, frames, smem + OFF_E + warp * PATCH_BYTES,
-                       *reinterpret_cast<Prep*>(smem + OFF_PREP + warp * (int)sizeof(Prep)));
+    if (prep_warp) {
+        // ======================= patch-preparation warps =======================
+        // producer of the two patch buffers: claims a strip, prepares its patches, publishes
+        // them (bar_full), and reuses a buffer once the data warps released it (bar_empty);
+        // a strip id < 0 ends the consumers' loop
+        Prep* const PB = reinterpret_cast<Prep*>(smem + OFF_PREP);   // [2][NC]
+        auto claim = [&](int& st, int& nc) {
+            if (tid == NPIPE) s_claim = (int)atomicAdd(&ctrl->strip_next, 1u);
+            tc05::named_sync(BAR_PREP, 32 * NPW);
+            st = s_claim;
+            nc = st < n_strips ? min(NC, n_cand - st * NC) : 0;
+            tc05::named_sync(BAR_PREP, 32 * NPW);             // s_claim read by all
+        };
+        int st, nc;
+        claim(st, nc);
+        if (nc > 0) prep_geometry(st * NC, nc, cands, lvinfo, frames, PB);
+        uint32_t uses[2] = {0u, 0u};
+        for (int it = 0;; ++it) {
+            const int b = it & 1;
+            if (uses[b] > 0) tc05::mbar_wait(&bar_empty[b], (uses[b] - 1u) & 1u);
+            ++uses[b];
+            int st_n = -1, nc_n = 0;
+            if (nc > 0) {
+                claim(st_n, nc_n);                             // the next strip: geometry + L2
+                if (nc_n > 0) prep_geometry(st_n * NC, nc_n, cands, lvinfo, frames, PB + (b ^ 1) * NC);
+                tc05::named_sync(BAR_PREP, 32 * NPW);
+#ifndef SELTC_SKIP_PREP                                         // timing experiments only
+                prep_sample(nc, smem + OFF_E + b * NC * PATCH_BYTES, PB + b * NC);
+#endif
+            }
+            if (tid == NPIPE) {
+                s_strip[b] = nc > 0 ? st : -1;
+                s_nc[b] = nc;
+            }
+            tc05::named_sync(BAR_PREP, 32 * NPW);              // patches and s_strip written
+            tc05::mbar_arrive(&bar_full[b]);
+            if (nc == 0) break;
+            st = st_n;
+            nc = nc_n;
         }
-        __syncthreads();
+    }
+    uint32_t uses[2] = {0u, 0u};
+    for (int it = 0; !prep_warp; ++it) {
+        const int b = it & 1;
+        tc05::mbar_wait(&bar_full[b], uses[b] & 1u);
+        ++uses[b];
+        const int st = s_strip[b];
+        if (st < 0) break;
+        const int c0 = st * NC;
+        const int nc = s_nc[b];
+#ifdef SELTC_SKIP_PIPE                                          // timing experiments only
+        if (!mma_warp) { __syncwarp(); if (lane == 0) tc05::mbar_arrive(&bar_empty[b]); }
+        continue;
+#endif
 
         if (!mma_warp) {
             // ============================ data warps ============================
             const bool slot_ok = slot < 2 * nc;
             const int orient = slot & 1;                       // 0 = E, 1 = M (mirror)
-            const uint8_t* prow = smem + OFF_E + (slot >> 1) * PATCH_BYTES;
-            // image row r of this lane's patch: pixels 4X .. 4X+7 (X = xp) as two words; the
-            // mirrored patch M(x) = E(50 - x) reverses the bytes of E words 11-X .. 13-X
+            const uint8_t* prow = smem + OFF_E + (b * NC + (slot >> 1)) * PATCH_BYTES;
+            const uint8_t* lut = reinterpret_cast<const Prep*>(smem + OFF_PREP)[b * NC + (slot >> 1)].lut;
+            auto eq = [&](uint32_t w) -> uint32_t {             // O6 equalisation of 4 pixels
+                return (uint32_t)lut[w & 0xFFu] | ((uint32_t)lut[(w >> 8) & 0xFFu] << 8) |
+                       ((uint32_t)lut[(w >> 16) & 0xFFu] << 16) | ((uint32_t)lut[w >> 24] << 24);
+            };
+            // image row r of this lane's patch: pixels 4X .. 4X+7 (X = xp) as two words of the
+            // sampled patch, equalised here; the mirrored patch M(x) = E(50 - x) reverses the
+            // bytes of words 11-X .. 13-X.  Pixel 51 (the pad) and the rows >= 55 reach only
+            // discarded outputs (zero weights or invalid rows)
             auto fetch = [&](int r, uint32_t (&pw)[2]) {
                 if (!slot_ok) { pw[0] = pw[1] = 0u; return; }
                 const uint32_t* rw = reinterpret_cast<const uint32_t*>(prow + min(r, ER - 1) * EP);
                 if (orient == 0) {
-                    pw[0] = rw[xp + 1];
-                    pw[1] = rw[xp + 2];
+                    pw[0] = eq(rw[xp + 1]);
+                    pw[1] = eq(rw[xp + 2]);
                 } else {
                     const uint32_t a = rw[11 - xp], b = rw[12 - xp], c = rw[13 - xp];
-                    pw[0] = __byte_perm(b, c, 0x3456);
-                    pw[1] = __byte_perm(a, b, 0x3456);
+                    pw[0] = eq(__byte_perm(b, c, 0x3456));
+                    pw[1] = eq(__byte_perm(a, b, 0x3456));
                 }
             };
             auto put = [&](int r, const uint32_t (&pw)[2]) {          // image row r -> ring slot r % 8
@@ -291,24 +393,18 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
             auto l1_epilogue = [&](int k) {
 #pragma unroll 1
                 for (int rr = 0; rr < 2; ++rr) {
-                    float d[64];
-                    {
-                        float a[32], b[32];
-                        ld32(tm + t_lane + TM_D1 + 128 * rr + 64 * hf, a);
-                        ld32(tm + t_lane + TM_D1 + 128 * rr + 64 * hf + 32, b);
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) { d[i] = a[i]; d[32 + i] = b[i]; }
-                    }
                     const int slot1 = (2 * k + rr) % P1_RING;
-#pragma unroll
+#pragma unroll 1
                     for (int cx = 0; cx < 2; ++cx) {
+                        float d[32];
+                        ld32(tm + t_lane + TM_D1 + 128 * rr + 64 * hf + 32 * cx, d);
                         uint32_t hi[4], lo[4];
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             float mx[2];
 #pragma unroll
                             for (int e = 0; e < 2; ++e) {
-                                const float* q = d + cx * 32 + 2 * c + e;
+                                const float* q = d + 2 * c + e;
                                 mx[e] = fmaxf(fmaxf(q[0], q[8]), fmaxf(q[16], q[24]));
                             }
                             const float2 x = __ffma2_rn(make_float2(mx[0], mx[1]), make_float2(K.l1s, K.l1s),
@@ -377,18 +473,23 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
                     acc3[mm][7] = 0.f;
                 }
                 const float r = act1(fmaf(K.w4[1], a.y, fmaf(K.w4[0], a.x, K.b4)));
-                if (e_col && o >= 0 && o < 5) rout[o * 5] = r;
+                if (e_col && o >= 0 && o < 5) {
+                    rout[o * 5] = r;
+                    if (r > sp.T2a) atomicAdd(&s_k2[b][slot >> 1], 1);    // K2
+                }
             };
             auto sync_for_mma = [&]() {
                 tc05::fence_async_smem();
                 tc05::fence_before();
-                tc05::cta_sync();
+                tc05::named_sync(BAR_PIPE, NPIPE);
             };
             auto wait_l1 = [&]() {
                 tc05::mbar_wait(&bar_l1, ph_l1 & 1); ++ph_l1;
                 tc05::fence_after();
             };
 
+            // K2 counters of this buffer (last read two strips ago, before the previous strip's syncs)
+            if (warp == 4 && lane < NC) s_k2[b][lane] = 0;
             // prologue: image rows 0..7 -> L1(0); rows 8..11 once unit 0 is drained; both
             // layer-2 halves zeroed before the first streamed MMAs.  The two warps of a lane
             // quadrant load the even / odd image rows.
@@ -450,6 +551,29 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
                 tc05::st_wait();
                 sync_for_mma();                                // -> L3(q-1), L1(q+2), L2s(q+1)
             }
+            // the equalised patches of the survivors the rule sends to CNN3 (K2 > 0 under Eq. 2,
+            // K2 < T_nn under Eq. 3; P:99 / S:358) -> epatch, for selective.cu
+            if (warp < nc) {
+                const int k2 = *(volatile int*)&s_k2[b][warp];
+                const bool need3 = sp.rule == 0 ? k2 > 0 : k2 < sp.Tnn;
+                if (need3) {
+                    const uint8_t* src = smem + OFF_E + (b * NC + warp) * PATCH_BYTES;
+                    const uint8_t* lt = reinterpret_cast<const Prep*>(smem + OFF_PREP)[b * NC + warp].lut;
+                    uint32_t* dst = reinterpret_cast<uint32_t*>(epatch + (int64_t)(c0 + warp) * kEPatchBytes);
+                    for (int wi = lane; wi < kEPatchBytes / 4; wi += 32) {
+                        uint32_t x = 0;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int k = min(4 * wi + q, kPatchN - 1);
+                            const int v = k / kPatchW, u = k - v * kPatchW;
+                            x |= (uint32_t)lt[src[v * EP + 4 + u]] << (8 * q);
+                        }
+                        dst[wi] = x;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) tc05::mbar_arrive(&bar_empty[b]);   // this strip's patches are read
         } else {
             // ============================ MMA warp ============================
             const uint64_t bd1 = tc05::sdesc(s_base + OFF_B1, 128 * 16, 128);
@@ -509,16 +633,16 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
                 }
                 __syncwarp();
             };
-            tc05::cta_sync();                                  // rows 0..7 in TMEM
+            tc05::named_sync(BAR_PIPE, NPIPE);                 // rows 0..7 in TMEM
             tc05::fence_after();
             issue_l1(0);
-            tc05::cta_sync();                                  // rows 8..11, P1 rows 0, 1, D2 zeroed
+            tc05::named_sync(BAR_PIPE, NPIPE);                 // rows 8..11, P1 rows 0, 1, D2 zeroed
             tc05::fence_after();
             issue_l1(1);
             issue_l2s(0);
 #pragma unroll 1
             for (int q = 0; q <= NQ + 1; ++q) {
-                tc05::cta_sync();
+                tc05::named_sync(BAR_PIPE, NPIPE);
                 tc05::fence_after();
                 if (q >= 1 && q <= NQ) issue_l3(q - 1);
                 if (q + 2 <= NQ) issue_l1(q + 2);
@@ -622,13 +746,14 @@ int selective_tc_bmats(const Cnn2W& w, uint16_t* out, Cnn2Tc* consts)
     return total;
 }
 
-void launch_selective_cnn2_tc(const Cnn2Tc& k, const uint16_t* d_bmats, const FrameInfo* d_frames,
-                              const LevelInfo* d_levels, const S1Cand* cands, uint32_t cand_cap,
-                              float* resp2, Ctrl* ctrl, int sm_count, cudaStream_t s)
+void launch_selective_cnn2_tc(const Cnn2Tc& k, SelParams sp, const uint16_t* d_bmats,
+                              const FrameInfo* d_frames, const LevelInfo* d_levels,
+                              const S1Cand* cands, uint32_t cand_cap, float* resp2, uint8_t* epatch,
+                              Ctrl* ctrl, int sm_count, cudaStream_t s)
 {
     cudaFuncSetAttribute(selective_cnn2_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    selective_cnn2_tc_kernel<<<sm_count, NT, SMEM_BYTES, s>>>(k, d_bmats, d_frames, d_levels, cands,
-                                                             cand_cap, resp2, ctrl);
+    selective_cnn2_tc_kernel<<<sm_count, NT, SMEM_BYTES, s>>>(k, sp, d_bmats, d_frames, d_levels, cands,
+                                                             cand_cap, resp2, epatch, ctrl);
 }
 
 }  // namespace ccnn

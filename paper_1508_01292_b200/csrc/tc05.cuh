@@ -100,6 +100,17 @@ __device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count)
 {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(mbar)), "r"(count) : "memory");
 }
+// plain arrive (release semantics at CTA scope): e.g. a producer warp publishing shared-memory data
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar)
+{
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}"
+                 :: "r"(smem_u32(mbar)) : "memory");
+}
+// named barrier `id` over `count` threads (warp multiples), non-aligned form
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t count)
+{
+    asm volatile("barrier.sync %0, %1;" :: "r"(id), "r"(count) : "memory");
+}
 __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ uint32_t mbar_try_wait(uint64_t* mbar, uint32_t parity)
 {
