@@ -181,6 +181,7 @@ void launch_stage1_tc(const Cnn1W& w, float T1, const uint16_t* d_bmats, const u
 int stage1_tc_band_width();
 int stage1_tc_grid(int sm_count);
 int stage1_tc_task_cost(int nrows);
+int stage1_tc_pipes_per_cta();    // band pipelines per CTA (each takes its own tasks)
 double stage1_tc_task_mma_flops(int nrows);
 int stage1_tc_bmats(const Cnn1W& w, uint16_t* out);   // fills out (kStage1TcBmatHalves), returns count
 constexpr int kStage1TcBmatHalves = 8 * 96 * 16 + 8 * 96 * 16 + 5 * 24 * 16;   // layers 1, 2, 3

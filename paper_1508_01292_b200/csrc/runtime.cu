@@ -556,7 +556,8 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
                 total += task_cost(t.nrows);
                 biggest = std::max<int64_t>(biggest, task_cost(t.nrows));
             }
-            if (biggest * c->s1_grid <= total) break;
+            const int64_t slots = (int64_t)c->s1_grid * (c->s1_tc ? stage1_tc_pipes_per_cta() : 1);
+            if (biggest * slots <= total) break;
         }
     }
     // tasks of all frames in one list, longest first (cost ~ super-steps, independent of the

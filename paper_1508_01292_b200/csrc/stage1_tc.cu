@@ -71,8 +71,12 @@ __device__ __forceinline__ float act1(float x)           // x' = 2x/3, one value
     return copysignf(fmaf(-1.7159f, r, 1.7159f), x);
 }
 
-constexpr int NW = 4;                   // data warps
-constexpr int NT = 32 * (NW + 1);       // + the MMA warp
+constexpr int NW = 4;                   // data warps of a pipeline
+constexpr int PWT = 32 * (NW + 1);      // threads of a pipeline (+ its MMA warp)
+constexpr int NPIPE = 2;                // independent band pipelines per CTA (one CTA per SM):
+                                        // they share one copy of the B matrices, so the SM keeps
+                                        // ~90 KB of L1 for the level loads and the overlapped pyramid
+constexpr int NT = NPIPE * PWT;
 constexpr int TW = 123;                 // windows per band (P2 columns 0..126 valid)
 // shared memory (bytes)
 constexpr int BMAT = 96 * 16 * 2;              // one layer-1 B (N = 96, K = 16): [k chunk 2][n 96][8]
@@ -90,16 +94,18 @@ constexpr int P2_E = 136;                      // P2 entries per (buffer, part):
 constexpr int P2_HL = P2_E * 16;
 constexpr int P2_BUF = 2 * P2_HL;
 constexpr int OFF_B1 = 0, OFF_B2 = OFF_B1 + B1_BYTES, OFF_B3 = OFF_B2 + B2_BYTES;
-constexpr int OFF_PL = OFF_B3 + B3_BYTES;
-constexpr int OFF_P2 = OFF_PL + P1_RING * PL_SLOT;
-constexpr int SMEM_BYTES = OFF_P2 + 2 * P2_BUF;
+constexpr int OFF_PL = OFF_B3 + B3_BYTES;      // per pipeline: P1 ring, then two P2 buffers
+constexpr int OFF_P2_REL = P1_RING * PL_SLOT;
+constexpr int PIPE_BYTES = OFF_P2_REL + 2 * P2_BUF;
+constexpr int SMEM_BYTES = OFF_PL + NPIPE * PIPE_BYTES;
 static_assert((B1_BYTES + B2_BYTES + B3_BYTES) / 2 == kStage1TcBmatHalves, "B matrix image size");
 // TMEM columns
 constexpr uint32_t TM_A = 0;                   // A ring: image row slot s at +4 s (32 columns)
 constexpr uint32_t TM_D1 = 32;                 // layer-1 accumulator (96)
 constexpr uint32_t TM_D2 = 128;                // layer-2 accumulators: [half 0 wh | half 1 wh | half 0 wl | half 1 wl]
 constexpr uint32_t TM_D3 = 224;                // layer-3 accumulator (24)
-constexpr uint32_t TM_COLS = 256;
+constexpr uint32_t TM_PIPE = 256;              // TMEM columns per pipeline
+constexpr uint32_t TM_COLS = TM_PIPE * NPIPE;
 constexpr uint32_t IDESC = tc05::idesc_f16(128, 96);
 constexpr uint32_t IDESC1_HALF = tc05::idesc_f16(128, 48);  // layer-1 row pairs 0 (P1 row 0), 3 (P1 row 1)
 constexpr uint32_t IDESC2 = tc05::idesc_f16(128, 96);
@@ -156,7 +162,7 @@ __device__ __forceinline__ void st_zero24(uint32_t taddr)
 }
 
 template <bool DEBUG>
-__global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
+__global__ void __launch_bounds__(NT, 1) stage1_tc_kernel(
     const __grid_constant__ Cnn1W W, const float T1, const uint16_t* __restrict__ bmats,
     const uint8_t* __restrict__ levels, const LevelInfo* __restrict__ lvinfo,
     const S1Task* __restrict__ tasks, const int32_t* __restrict__ cta_first,
@@ -164,16 +170,17 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     float* __restrict__ dbg_map)
 {
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ int s_task;
+    __shared__ int s_task[NPIPE];
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) uint64_t bar_l1, bar_l2, bar_l3;
+    __shared__ __align__(8) uint64_t bar_l1s[NPIPE], bar_l2s[NPIPE], bar_l3s[NPIPE];
 
     const int tid = threadIdx.x;
     // warp index through shfl: provably warp-uniform, so role branches stay on the uniform
     // datapath (constant-bank weights via LDCU [UR+imm], MMA descriptors in uniform registers)
     const int warp = __shfl_sync(0xFFFFFFFFu, tid >> 5, 0);
     const int lane = tid & 31;
-    const bool mma_warp = warp == NW;
+    const int pipe = warp / (NW + 1);          // band pipeline of this warp
+    const bool mma_warp = warp - pipe * (NW + 1) == NW;
 
     // ---- one-time setup: weights (B matrices) to shared memory, zeroed plane padding ----
     {
@@ -183,18 +190,27 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
         uint4* z = reinterpret_cast<uint4*>(smem + OFF_PL);
         for (int i = tid; i < (SMEM_BYTES - OFF_PL) / 16; i += NT) z[i] = make_uint4(0, 0, 0, 0);
     }
-    if (mma_warp) tc05::tmem_alloc(&s_tmem, TM_COLS);
+    if (warp == NW) tc05::tmem_alloc(&s_tmem, TM_COLS);
     if (tid == 0) {
-        tc05::mbar_init(&bar_l1, 1);
-        tc05::mbar_init(&bar_l2, 1);
-        tc05::mbar_init(&bar_l3, 1);
+        for (int p = 0; p < NPIPE; ++p) {
+            tc05::mbar_init(&bar_l1s[p], 1);
+            tc05::mbar_init(&bar_l2s[p], 1);
+            tc05::mbar_init(&bar_l3s[p], 1);
+        }
         tc05::mbar_fence_init();
     }
     tc05::fence_async_smem();
     tc05::fence_before();
     __syncthreads();
     tc05::fence_after();
-    const uint32_t tm = s_tmem;
+    const uint32_t tm = s_tmem + TM_PIPE * (uint32_t)pipe;
+    uint64_t& bar_l1 = bar_l1s[pipe];
+    uint64_t& bar_l2 = bar_l2s[pipe];
+    uint64_t& bar_l3 = bar_l3s[pipe];
+    const int OFF_P1P = OFF_PL + pipe * PIPE_BYTES;            // this pipeline's P1 ring
+    const int OFF_P2P = OFF_P1P + OFF_P2_REL;                  // ... and P2 buffers
+    const uint32_t pbar = 1u + (uint32_t)pipe;                 // its named barrier
+    auto pipe_sync = [pbar] { tc05::named_sync(pbar, PWT); };
     // completed phases of each mbarrier (the waiting side's count)
     uint32_t ph_l1 = 0, ph_l2 = 0, ph_l3 = 0;
 
@@ -204,9 +220,9 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
 
     const int n_tasks = cta_first[gridDim.x];
     for (;;) {
-        if (tid == 0) s_task = (int)atomicAdd(&ctrl->task_next, 1u);
-        __syncthreads();
-        const int ti = s_task;
+        if (tid == pipe * PWT) s_task[pipe] = (int)atomicAdd(&ctrl->task_next, 1u);
+        pipe_sync();
+        const int ti = s_task[pipe];
         if (ti >= n_tasks) break;
         const S1Task T = tasks[ti];
         const int nrows = T.nrows;
@@ -271,7 +287,7 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                             split_h2(act2(x), hi[c], lo[c]);
                         }
                         const int slot = (2 * k + rr) % P1_RING;
-                        uint8_t* e = smem + OFF_PL + slot * PL_SLOT + cx * PL_PAR + m * 16;
+                        uint8_t* e = smem + OFF_P1P + slot * PL_SLOT + cx * PL_PAR + m * 16;
                         *reinterpret_cast<uint4*>(e) = make_uint4(hi[0], hi[1], hi[2], 0u);
                         *reinterpret_cast<uint4*>(e + PL_HL) = make_uint4(lo[0], lo[1], lo[2], 0u);
                     }
@@ -300,7 +316,7 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                                                 make_float2(W.tcx[6 + 2 * c], W.tcx[7 + 2 * c]));
                     split_h2(act2(x), hi[c], lo[c]);
                 }
-                uint8_t* e = smem + OFF_P2 + (q & 1) * P2_BUF + m * 16;
+                uint8_t* e = smem + OFF_P2P + (q & 1) * P2_BUF + m * 16;
                 *reinterpret_cast<uint4*>(e) = make_uint4(hi[0], hi[1], hi[2], 0u);
                 *reinterpret_cast<uint4*>(e + P2_HL) = make_uint4(lo[0], lo[1], lo[2], 0u);
             };
@@ -370,7 +386,7 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
             auto sync_for_mma = [&]() {
                 tc05::fence_async_smem();
                 tc05::fence_before();
-                tc05::cta_sync();
+                pipe_sync();
             };
             auto wait_l1 = [&]() {
                 tc05::mbar_wait(&bar_l1, ph_l1 & 1); ++ph_l1;
@@ -441,9 +457,9 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
             // ============================ MMA warp ============================
             const uint64_t bd1 = tc05::sdesc(s_base + OFF_B1, 96 * 16, 128);
             const uint64_t bd2 = tc05::sdesc(s_base + OFF_B2, 96 * 16, 128);
-            const uint64_t ad2 = tc05::sdesc(s_base + OFF_PL, PL_PAR, 128);
+            const uint64_t ad2 = tc05::sdesc(s_base + OFF_P1P, PL_PAR, 128);
             const uint64_t bd3 = tc05::sdesc(s_base + OFF_B3, 24 * 16, 128);
-            const uint64_t ad3 = tc05::sdesc(s_base + OFF_P2, P2_HL, 128);
+            const uint64_t ad3 = tc05::sdesc(s_base + OFF_P2P, P2_HL, 128);
             // layer 1 of unit k: row pair 1 first (N = 96, initialises the accumulator), then
             // pairs 2 (N = 96), 0 (P1 row 0 only) and 3 (P1 row 1 only) at N = 48
             auto issue_l1 = [&](int k) {
@@ -498,16 +514,16 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
                 }
                 __syncwarp();
             };
-            tc05::cta_sync();                                  // rows 0..7 in TMEM
+            pipe_sync();                                       // rows 0..7 in TMEM
             tc05::fence_after();
             issue_l1(0);
-            tc05::cta_sync();                                  // rows 8..11, P1 rows 0, 1, D2 zeroed
+            pipe_sync();                                       // rows 8..11, P1 rows 0, 1, D2 zeroed
             tc05::fence_after();
             issue_l1(1);
             issue_l2s(0);
 #pragma unroll 1
             for (int q = 0; q <= NQ + 1; ++q) {
-                tc05::cta_sync();
+                pipe_sync();
                 tc05::fence_after();
                 if (q >= 1 && q <= NQ) issue_l3(q - 1);
                 if (q + 2 <= NQ) issue_l1(q + 2);
@@ -518,12 +534,19 @@ __global__ void __launch_bounds__(NT, 2) stage1_tc_kernel(
     tc05::fence_before();
     __syncthreads();
     tc05::fence_after();
-    if (mma_warp) tc05::tmem_dealloc(tm, TM_COLS);
+    if (warp == NW) tc05::tmem_dealloc(s_tmem, TM_COLS);
 }
 
-// shared-memory carveout: 2 CTAs x 93 KB fit the 196 KB configuration (86% of 228 KB); the rest
-// of the unified L1 stays cache for the level loads and the overlapped pyramid (K1)
-constexpr int kCarveoutPct = 86;
+// shared-memory carveout: one CTA of two pipelines (135 KB) fits the 164 KB configuration (72% of
+// 228 KB); the rest of the unified L1 (~90 KB) stays cache for the level loads and the
+// overlapped pyramid's byte gathers (K1)
+#ifndef S1_CARVEOUT                            // experiments: -DS1_CARVEOUT=50 -DS1_MAX_CTAS=1
+#define S1_CARVEOUT 72
+#endif
+#ifndef S1_MAX_CTAS
+#define S1_MAX_CTAS 1
+#endif
+constexpr int kCarveoutPct = S1_CARVEOUT;
 
 template <bool DEBUG>
 int occupancy()
@@ -542,7 +565,7 @@ int occupancy()
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     occ = std::max(occ, smem_sm / (SMEM_BYTES + 128 + 1024));
-    occ = std::min(occ, 2);                  // TMEM: 256 columns per CTA
+    occ = std::min(occ, S1_MAX_CTAS);        // TMEM: 512 columns per CTA (two pipelines)
     return occ < 1 ? 1 : occ;
 }
 
@@ -551,6 +574,7 @@ int occupancy()
 int stage1_tc_band_width() { return TW; }
 int stage1_tc_grid(int sm_count) { return sm_count * std::min(occupancy<false>(), occupancy<true>()); }
 int stage1_tc_task_cost(int nrows) { return nrows + 5 + 2; }
+int stage1_tc_pipes_per_cta() { return NPIPE; }
 // tensor-core FLOPs (2 M N K per MMA) the kernel issues for a task of nrows window rows:
 // NQ + 1 layer-1 units and streamed layer-2 P1-row pairs, NQ layer-3 P2 rows (NQ = nrows + 5)
 double stage1_tc_task_mma_flops(int nrows)
