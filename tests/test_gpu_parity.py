@@ -575,3 +575,32 @@ def test_rgb_ingest(ws, cascade):
     with pytest.raises(ccnn.CcnnError) as e:
         det.detect_frames([np.zeros((40, 40, 2), np.uint8)], 20, 1.15)
     assert e.value.code == ccnn.CCNN_E_ARG
+
+
+def test_fp32_ffma_vs_split_fp16_tcgen05_precision(ws, cascade, monkeypatch):
+    """north_star names an fp32 FMA path for stage 1; the product kernel runs the three conv
+    layers as fp16 hi+lo split tcgen05 MMAs with fp32 accumulation.  Side by side on the same
+    frames (two 1080p frames, every window of every level): both kernels' dense stage-1 maps
+    against the fp64 oracle, and against each other.  Both must meet the 1e-4 bar; the split
+    form's error is reported (profiles/r2_precision.txt records a run)."""
+    from paper_1508_01292_b200 import ccnn
+    c = configs.C3
+    fr = c.make_frames(2)
+    T1, T2 = c.thresholds()
+    lv, maps = parity.oracle_maps(cascade, fr, c.min_face, c.scale_step)
+    got = {}
+    for legacy in ("0", "1"):
+        monkeypatch.setenv("CCNN_S1_LEGACY", legacy)
+        det = make_det(ws, T1, T2, c.Tnn, c.rule, max_batch=2)
+        det.set_debug(ccnn.CCNN_DEBUG_STAGE1)
+        det.detect(fr, c.min_face, c.scale_step)
+        got[legacy] = {k: det.stage1_map(*k).astype(np.float64) for k in maps}
+        det.close()
+    err = {}
+    for legacy in ("0", "1"):
+        err[legacy] = max(float(np.max(np.abs(got[legacy][k] - maps[k]))) for k in maps if maps[k].size)
+    between = max(float(np.max(np.abs(got["0"][k] - got["1"][k]))) for k in maps if maps[k].size)
+    n = sum(m.size for m in maps.values())
+    print(f"windows {n}: max |tcgen05 split-fp16 - fp64 oracle| = {err['0']:.3e}, "
+          f"max |FFMA fp32 - fp64 oracle| = {err['1']:.3e}, max |tcgen05 - FFMA| = {between:.3e}")
+    assert err["0"] <= parity.TOL and err["1"] <= parity.TOL
