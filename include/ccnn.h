@@ -76,7 +76,7 @@ typedef struct {
     int32_t rule;              /* 0 = Eq. 2 strict, 1 = Eq. 3 weak             */
     int32_t nms_min_cluster;   /* drop groups smaller than this (O9; default 1)               */
     int32_t max_w, max_h;      /* largest frame accepted by ccnn_detect                        */
-    int32_t max_batch;         /* largest n accepted by ccnn_detect                            */
+    int32_t max_batch;         /* largest n accepted by ccnn_detect (1 .. 4096)                */
     int32_t queue_capacity;    /* stage-1 survivor records per frame (S:430 default 4096)     */
     int32_t segment_rows;      /* stage-1 task height in window rows (0 = adaptive)            */
 } ccnn_params;

@@ -207,14 +207,48 @@ __global__ void __launch_bounds__(kNmsThreads) nms_kernel(
     __syncthreads();
     if (!sm.is_last) return;
     __threadfence();
+    // frame offsets: block-wide exclusive scan of the frame counts, kNmsThreads frames per pass
+    // (all loads issued together -- a serial walk over the frames was a chain of dependent
+    // global loads, ~1 us each), into sm.sx[] (the frames' first output index) -- then every
+    // output box is copied by its own thread (binary search for its frame)
+    const int lane = tid & 31, wid = tid >> 5;
     int base = 0;
-    for (int g = 0; g < n_frames; ++g) {
-        const int c = *(volatile int32_t*)&frame_counts[g];
-        const OutBox* src = staging + (int64_t)g * 2 * kNmsCap + kNmsCap;
-        for (int k = tid; k < c; k += kNmsThreads) out[base + k] = src[k];
-        base += c;
+    for (int g0 = 0; g0 < n_frames; g0 += kNmsThreads) {
+        const int g = g0 + tid;
+        const int c = g < n_frames ? *(volatile int32_t*)&frame_counts[g] : 0;
+        int x = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int t = __shfl_up_sync(0xFFFFFFFFu, x, d);
+            if (lane >= d) x += t;
+        }
+        if (lane == 31) sm.sy[wid] = x;                       // warp totals
+        __syncthreads();
+        if (wid == 0) {
+            int w = lane < kNmsThreads / 32 ? sm.sy[lane] : 0;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int t = __shfl_up_sync(0xFFFFFFFFu, w, d);
+                if (lane >= d) w += t;
+            }
+            if (lane < kNmsThreads / 32) sm.sw[lane] = w;      // inclusive warp prefix
+        }
+        __syncthreads();
+        const int incl = x + (wid > 0 ? sm.sw[wid - 1] : 0);
+        if (g < n_frames) sm.sx[g] = base + incl - c;          // n_frames <= kNmsCap (ccnn_create)
+        base += sm.sw[kNmsThreads / 32 - 1];
+        __syncthreads();
     }
-    if (tid == 0) ctrl->n_out = (uint32_t)base;
+    const int total = base;
+    for (int i = tid; i < total; i += kNmsThreads) {
+        int lo = 0, hi = n_frames - 1;                        // last frame with offset <= i
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sm.sx[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        out[i] = staging[(int64_t)lo * 2 * kNmsCap + kNmsCap + (i - sm.sx[lo])];
+    }
+    if (tid == 0) ctrl->n_out = (uint32_t)total;
 }
 
 }  // namespace

@@ -603,7 +603,8 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
         if (!p->net[k].weights || !finite_all(p->net[k].weights, p->net[k].n_weights)) return CCNN_E_WEIGHTS;
     if (!std::isfinite(p->T1) || !std::isfinite(p->T2[0]) || !std::isfinite(p->T2[1])) return CCNN_E_WEIGHTS;
     if (p->Tnn < 1 || (p->rule != 0 && p->rule != 1) || p->max_w < kWinW || p->max_h < kWinH ||
-        p->max_w > 16384 || p->max_h > 16384 || p->max_batch < 1 || p->queue_capacity < 0 ||
+        p->max_w > 16384 || p->max_h > 16384 || p->max_batch < 1 || p->max_batch > kNmsCap ||
+        p->queue_capacity < 0 ||
         p->nms_min_cluster < 0 || p->segment_rows < 0)
         return CCNN_E_ARG;
     int ndev = 0;
