@@ -86,6 +86,8 @@ struct ccnn_ctx {
     std::vector<int32_t> cta_first;     // stage1_grid + 1 offsets into tasks
     int s1_grid = 0;
     bool s1_tc = true;                  // stage 1 on tcgen05 (stage1_tc.cu); CCNN_S1_LEGACY=1 -> stage1.cu
+    bool patchwork = true;              // pack levels' tail pieces into shared bands;
+                                        // CCNN_PATCHWORK=0: one band per tail (the ablation)
     DevBuf s1_bmats;                    // its B matrices
     DevBuf sel_bmats;                   // selective CNN2 (tcgen05) B matrices
     Cnn2Tc sel_consts{};                // ... and epilogue constants
@@ -511,7 +513,7 @@ void build_plan(ccnn_ctx* c, const PlanKey& key)
     const size_t first_tail_band = bands.size();
     for (const S1Piece& t : tails) {
         bool placed = false;
-        for (size_t k = first_tail_band; k < bands.size() && !placed; ++k) {
+        for (size_t k = first_tail_band; c->patchwork && k < bands.size() && !placed; ++k) {
             Band& b = bands[k];
             if (b.npieces < kMaxPieces && b.used + kPieceGap + t.w <= TW) {
                 S1Piece p = t;
@@ -631,6 +633,8 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
     {
         const char* leg = std::getenv("CCNN_S1_LEGACY");
         ctx->s1_tc = !(leg && leg[0] == '1');
+        const char* pw = std::getenv("CCNN_PATCHWORK");
+        ctx->patchwork = !(pw && pw[0] == '0');
     }
     ctx->s1_grid = ctx->s1_tc ? stage1_tc_grid(ctx->sm_count) : stage1_grid(ctx->sm_count);
     if (const char* v = std::getenv("CCNN_VERBOSE"))
