@@ -44,17 +44,12 @@ struct __align__(16) Cnn1W {   // 797 weights + re-arranged copies for the stage
 };
 template <int A, int B, int C>
 struct __align__(16) SelNetW { // CNN2: <16,6,2>, CNN3: <2,2,25>
-    static constexpr int W2V = (B * 9 + 3) / 4 * 4;
-    float w2v[A][W2V];         // layer 2 per input map a: [(ky*3 + kx)*B + b] (map pairs adjacent
-                               // for the f32x2 FMAs), float4 blocks
     float w1[A][16], b1[A];
     float w2[B][A][9], b2[B];
     float w3[C][B][56], b3[C]; // [out][in][ky*7+kx], 7 wide x 8 tall
     float w4[C], b4;
-    // layer 1 on the tensor cores (selective.cu, A == 16): mma.m16n8k16 B fragments of
-    // w1 / 127.5 * 2^s (raw equalised pixels in, O3 folded) as fp16 hi + lo,
-    // [hi/lo][map half][lane][reg]; b1h = b1 - sum_k w1; accumulator scaled by l1_inv_scale
-    uint32_t l1frag[2][2][32][2];
+    // O3 folded into layer 1 (raw equalised pixels in): b1h = b1 - sum_k w1, and the power of
+    // two that scales w1 / 127.5 into fp16 range for the tensor-core copies (selective_tc.cu)
     float b1h[A];
     float l1_inv_scale;
 };

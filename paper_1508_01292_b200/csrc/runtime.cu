@@ -284,32 +284,11 @@ void unpack_sel(const float* p, SelNetW<A, B, C>& o)
     std::memcpy(o.b3, p, sizeof(o.b3)); p += C;
     std::memcpy(o.w4, p, sizeof(o.w4)); p += C;
     o.b4 = *p;
-    for (int a = 0; a < A; ++a)
-        for (int k = 0; k < SelNetW<A, B, C>::W2V; ++k)
-            o.w2v[a][k] = k < B * 9 ? o.w2[k % B][a][k / B] : 0.f;
-    // tensor-core layer-1 fragments (used for A == 16): N = 16 maps as two halves of 8
     double mx = 0.0;
     for (int a = 0; a < A; ++a)
         for (int k = 0; k < 16; ++k) mx = std::max(mx, std::fabs((double)o.w1[a][k]) / 127.5);
     const int e = mx > 0.0 ? (int)std::floor(std::log2(mx)) : 0;
-    const double sc = std::ldexp(1.0, 3 - e);
     o.l1_inv_scale = (float)std::ldexp(1.0, e - 3);
-    auto part = [&](int n, int k, int lo) -> uint16_t {
-        if (n >= A) return 0;
-        const float wp = (float)((double)o.w1[n][k] / 127.5 * sc);
-        const __half hi = __float2half_rn(wp);
-        if (!lo) return __half_as_ushort(hi);
-        return __half_as_ushort(__float2half_rn(wp - __half2float(hi)));
-    };
-    for (int lo = 0; lo < 2; ++lo)
-        for (int nh = 0; nh < 2; ++nh)
-            for (int lane = 0; lane < 32; ++lane) {
-                const int n = 8 * nh + lane / 4, k0 = (lane % 4) * 2;
-                for (int r = 0; r < 2; ++r) {
-                    const int k = k0 + 8 * r;
-                    o.l1frag[lo][nh][lane][r] = (uint32_t)part(n, k, lo) | ((uint32_t)part(n, k + 1, lo) << 16);
-                }
-            }
     for (int a = 0; a < A; ++a) {
         double b = (double)o.b1[a];
         for (int k = 0; k < 16; ++k) b -= (double)o.w1[a][k];
