@@ -139,12 +139,11 @@ def bind_host_to_gpu(dev_index):
     socket interconnect).  Returns (previous affinity or None, outcome text)."""
     try:
         import torch
-        uuid = str(torch.cuda.get_device_properties(dev_index).uuid)
-        bus = subprocess.run(["nvidia-smi", "-i", "GPU-" + uuid, "--query-gpu=pci.bus_id",
-                              "--format=csv,noheader"], capture_output=True, text=True,
-                             timeout=20).stdout.strip().lower()
-        if bus.count(":") == 2 and len(bus.split(":")[0]) == 8:
-            bus = bus[4:]                                  # 00000000:1b:00.0 -> 0000:1b:00.0
+        # the PCI address from the CUDA device properties, not an nvidia-smi subprocess: a
+        # driver query from another process right before the e2e loop was measured to slow
+        # the loop's H2D copies (tools/e2e_probe.py: 6.6k -> 4.5k frames/s at C4)
+        p = torch.cuda.get_device_properties(dev_index)
+        bus = "%04x:%02x:%02x.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
         with open(f"/sys/bus/pci/devices/{bus}/local_cpulist") as f:
             cpus = parse_cpulist(f.read())
         old = os.sched_getaffinity(0)
@@ -444,10 +443,10 @@ def main():
     # ---- e2e: the streaming public API (ccnn_submit / ccnn_collect) with the frames in
     #      pinned HOST memory: every step copies its frames H2D and reads its boxes back;
     #      the copy of step k+1 overlaps the kernels of step k (three batches in flight) ----
-    # enough steps for a >= ~100 ms e2e region (host jitter of a few ms must not dominate a
+    # enough steps for a >= ~300 ms e2e region (host jitter of a few ms must not dominate a
     # small config's rate): estimate a step from the device-timed loop + H2D at ~40 GB/s
     est_ms = ms / args.steps + frames.nbytes / 40e9 * 1e3
-    e2e_steps = args.e2e_steps or int(min(2000, max(10, args.steps, np.ceil(100.0 / max(est_ms, 1e-3)))))
+    e2e_steps = args.e2e_steps or int(min(2000, max(10, args.steps, np.ceil(300.0 / max(est_ms, 1e-3)))))
     # per-stage device times of synchronous calls (no neighbouring batches on the GPU): what
     # each kernel costs alone, e.g. the pyramid's bandwidth (outside the timed regions)
     alone = []

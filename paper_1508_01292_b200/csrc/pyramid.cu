@@ -239,7 +239,10 @@ __device__ __forceinline__ void load_cols(const uint32_t* __restrict__ xt, int t
 
 // GATHER class, SAFE tables (W, H >= 2: x0 + 1, y0 + 1 always inside): 4 byte gathers per
 // pixel from the frame through L1
-__global__ void __launch_bounds__(kPyrCols) pyramid_gather4_kernel(
+#ifndef PYR_MINB
+#define PYR_MINB 1
+#endif
+__global__ void __launch_bounds__(kPyrCols, PYR_MINB) pyramid_gather4_kernel(
     const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
     const LevelInfo* __restrict__ lv, const uint32_t* __restrict__ tiles,
     const uint32_t* __restrict__ tabs)

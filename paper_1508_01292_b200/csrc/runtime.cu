@@ -123,6 +123,9 @@ struct ccnn_ctx {
                                     // selective unit / NMS of batch k (tail stream) overlap
                                     // the stage 1 of batch k+1 (compute stream)
         Ctrl* h_ctrl = nullptr;     // pinned readback of ctrl
+        std::vector<FrameInfo> fi_dev;  // what finfo holds on the device (skip identical uploads:
+        const void* fi_dev_p = nullptr; // a small H2D queued behind the next batch's frame copy
+                                        // on the copy engine would hold up this batch's pyramid)
         cudaEvent_t ev[9] = {};     // h2d0, h2d1, c0, pyramid, stage1, selective, end, stage-1 start,
                                     // selective start
         cudaEvent_t ev_user = nullptr;  // ctx stream at submit (orders the H2D of host frames)
@@ -928,7 +931,13 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     cudaStream_t ps = ctx->pyr_stream;
     CU(cudaStreamWaitEvent(ps, sl.ev[1], 0));
     if (sl.used) CU(cudaStreamWaitEvent(ps, sl.ev[4], 0));
-    CU(cudaMemcpyAsync(sl.finfo.p, fi, sizeof(FrameInfo) * n, cudaMemcpyHostToDevice, ps));
+    if (sl.fi_dev_p != sl.finfo.p || sl.fi_dev.size() != (size_t)n ||
+        std::memcmp(sl.fi_dev.data(), fi, sizeof(FrameInfo) * n) != 0) {
+        sl.fi_dev_p = nullptr;
+        CU(cudaMemcpyAsync(sl.finfo.p, fi, sizeof(FrameInfo) * n, cudaMemcpyHostToDevice, ps));
+        sl.fi_dev.assign(fi, fi + n);
+        sl.fi_dev_p = sl.finfo.p;
+    }
     const FrameInfo* dfi = sl.finfo.as<FrameInfo>();
     CU(cudaEventRecord(sl.ev[2], ps));
     if (ctx->epoch == nullptr && std::getenv("CCNN_TIMELINE")) {
@@ -1038,11 +1047,11 @@ int ccnn_collect(ccnn_ctx* ctx, ccnn_box* boxes, int64_t box_cap, int64_t* n_box
         }
     }
     if (ctx->epoch && sl.timed) {          // timeline diagnostics (ms since the first pyramid)
-        const int ids[6] = {2, 3, 7, 4, 5, 6};
-        float t[6] = {};
-        for (int k = 0; k < 6; ++k) cudaEventElapsedTime(&t[k], ctx->epoch, sl.ev[ids[k]]);
-        std::fprintf(stderr, "ccnn timeline batch %lld: pyr %.4f-%.4f s1 %.4f-%.4f sel-%.4f end %.4f\n",
-                     (long long)ctx->batch_no, t[0], t[1], t[2], t[3], t[4], t[5]);
+        const int ids[8] = {2, 3, 7, 4, 5, 6, 0, 1};
+        float t[8] = {};
+        for (int k = 0; k < 8; ++k) cudaEventElapsedTime(&t[k], ctx->epoch, sl.ev[ids[k]]);
+        std::fprintf(stderr, "ccnn timeline batch %lld: pyr %.4f-%.4f s1 %.4f-%.4f sel-%.4f end %.4f h2d %.4f-%.4f\n",
+                     (long long)ctx->batch_no, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
     }
     ++ctx->batch_no;
     *n_boxes = hc.n_out;

@@ -162,7 +162,10 @@ __device__ __forceinline__ void st_zero24(uint32_t taddr)
 }
 
 template <bool DEBUG>
-__global__ void __launch_bounds__(NT, 1) stage1_tc_kernel(
+#ifndef S1_MINB
+#define S1_MINB 1
+#endif
+__global__ void __launch_bounds__(NT, S1_MINB) stage1_tc_kernel(
     const __grid_constant__ Cnn1W W, const float T1, const uint16_t* __restrict__ bmats,
     const uint8_t* __restrict__ levels, const LevelInfo* __restrict__ lvinfo,
     const S1Task* __restrict__ tasks, const int32_t* __restrict__ cta_first,
