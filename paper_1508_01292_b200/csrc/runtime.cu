@@ -65,6 +65,8 @@ bool finite_all(const float* w, int64_t n)
 struct ccnn_ctx {
     int device = 0;
     int sm_count = 148;
+    int sel_grid = 0;                   // selective CNN2 grid (0 = sm_count; CCNN_SEL_GRID, experiments)
+    int cnn3_grid = 0;                  // CNN3 + rule grid in SMs (0 = sm_count; CCNN_CNN3_SMS)
     cudaStream_t stream = nullptr;
     std::string err;
     int debug = 0;
@@ -598,6 +600,8 @@ int ccnn_create(const ccnn_params* p, int cuda_device, ccnn_ctx** out)
     ctx->device = cuda_device;
     CU(cudaSetDevice(cuda_device));
     CU(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, cuda_device));
+    if (const char* e = std::getenv("CCNN_SEL_GRID")) ctx->sel_grid = std::atoi(e);
+    if (const char* e = std::getenv("CCNN_CNN3_SMS")) ctx->cnn3_grid = std::atoi(e);
     unpack_cnn1(p->net[0].weights, ctx->w1);
     unpack_sel(p->net[1].weights, ctx->w2);
     unpack_sel(p->net[2].weights, ctx->w3);
@@ -972,11 +976,12 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     CU(cudaEventRecord(sl.ev[8], ts));
     launch_selective_cnn2_tc(ctx->sel_consts, ctx->sp, ctx->sel_bmats.as<uint16_t>(), dfi,
                              ctx->d_levels.as<LevelInfo>(), sl.cands.as<S1Cand>(), cand_cap,
-                             sl.resp2.as<float>(), sl.epatch.as<uint8_t>(), dctrl, ctx->sm_count, ts);
+                             sl.resp2.as<float>(), sl.epatch.as<uint8_t>(), dctrl,
+                             ctx->sel_grid > 0 ? ctx->sel_grid : ctx->sm_count, ts);
     launch_selective(ctx->w3, ctx->sp, ctx->d_levels.as<LevelInfo>(), sl.cands.as<S1Cand>(), cand_cap,
                      sl.resp2.as<float>(), sl.epatch.as<uint8_t>(), sl.selout.as<SelOut>(),
                      dbg1 ? ctx->dbg_resp.as<float>() : nullptr, sl.acc.as<AccBox>(), dctrl,
-                     ctx->sm_count, ts);
+                     ctx->cnn3_grid > 0 ? ctx->cnn3_grid : ctx->sm_count, ts);
     CU(cudaEventRecord(sl.ev[5], ts));
     launch_nms(sl.acc.as<AccBox>(), dctrl, n, ctx->min_cluster, sl.staging.as<OutBox>(),
                sl.counts.as<int32_t>(), sl.out.as<OutBox>(), ts);

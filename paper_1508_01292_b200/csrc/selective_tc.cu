@@ -170,7 +170,7 @@ __device__ __forceinline__ void st_zero24(uint32_t taddr)
 // preparation warps, in two parts: prep_geometry (O5 sampling tables of every patch column /
 // row; run one strip ahead, while the previous strip's sampling is still to come) and prep_sample (O2
 // sampling into the 56 x 64-B patch rows at ebuf -- pixel x of row y at byte y*64 + 4 + x --,
-// histogram, O6 LUT; the data warps equalise the pixels as they load them)
+// histogram, O6 LUT, equalisation in place)
 __device__ __forceinline__ void prep_geometry(int c0, int nc, const S1Cand* __restrict__ cands,
                                               const LevelInfo* __restrict__ lvinfo,
                                               const FrameInfo* __restrict__ frames, Prep* P)
@@ -248,6 +248,18 @@ __device__ __forceinline__ void prep_sample(int nc, uint8_t* ebuf, Prep* P)
     }
     psync();
     for (int c = pt >> 5; c < nc; c += NPW) sel::warp_lut(P[c].hist, P[c].lut);
+    psync();
+    // O6 applied in place, 4 pixels per word (rows 0..54; the pad bytes of a row only reach
+    // discarded outputs): the data warps and the CNN3 copy then read E directly
+    constexpr int RW = EP / 4;
+    for (int i = pt; i < nc * kPatchH * RW; i += 32 * NPW) {
+        const int c = i / (kPatchH * RW), k = i - c * (kPatchH * RW);
+        uint32_t* w = reinterpret_cast<uint32_t*>(ebuf + c * PATCH_BYTES) + k;
+        const uint8_t* lut = P[c].lut;
+        const uint32_t x = *w;
+        *w = (uint32_t)lut[x & 0xFFu] | ((uint32_t)lut[(x >> 8) & 0xFFu] << 8) |
+             ((uint32_t)lut[(x >> 16) & 0xFFu] << 16) | ((uint32_t)lut[x >> 24] << 24);
+    }
     psync();
 }
 
@@ -363,25 +375,20 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
             const bool slot_ok = slot < 2 * nc;
             const int orient = slot & 1;                       // 0 = E, 1 = M (mirror)
             const uint8_t* prow = smem + OFF_E + (b * NC + (slot >> 1)) * PATCH_BYTES;
-            const uint8_t* lut = reinterpret_cast<const Prep*>(smem + OFF_PREP)[b * NC + (slot >> 1)].lut;
-            auto eq = [&](uint32_t w) -> uint32_t {             // O6 equalisation of 4 pixels
-                return (uint32_t)lut[w & 0xFFu] | ((uint32_t)lut[(w >> 8) & 0xFFu] << 8) |
-                       ((uint32_t)lut[(w >> 16) & 0xFFu] << 16) | ((uint32_t)lut[w >> 24] << 24);
-            };
             // image row r of this lane's patch: pixels 4X .. 4X+7 (X = xp) as two words of the
-            // sampled patch, equalised here; the mirrored patch M(x) = E(50 - x) reverses the
-            // bytes of words 11-X .. 13-X.  Pixel 51 (the pad) and the rows >= 55 reach only
-            // discarded outputs (zero weights or invalid rows)
+            // equalised patch E; the mirrored patch M(x) = E(50 - x) reverses the bytes of words
+            // 11-X .. 13-X.  Pixel 51 (the pad) and the rows >= 55 reach only discarded outputs
+            // (zero weights or invalid rows)
             auto fetch = [&](int r, uint32_t (&pw)[2]) {
                 if (!slot_ok) { pw[0] = pw[1] = 0u; return; }
                 const uint32_t* rw = reinterpret_cast<const uint32_t*>(prow + min(r, ER - 1) * EP);
                 if (orient == 0) {
-                    pw[0] = eq(rw[xp + 1]);
-                    pw[1] = eq(rw[xp + 2]);
+                    pw[0] = rw[xp + 1];
+                    pw[1] = rw[xp + 2];
                 } else {
                     const uint32_t a = rw[11 - xp], b = rw[12 - xp], c = rw[13 - xp];
-                    pw[0] = eq(__byte_perm(b, c, 0x3456));
-                    pw[1] = eq(__byte_perm(a, b, 0x3456));
+                    pw[0] = __byte_perm(b, c, 0x3456);
+                    pw[1] = __byte_perm(a, b, 0x3456);
                 }
             };
             auto put = [&](int r, const uint32_t (&pw)[2]) {          // image row r -> ring slot r % 8
@@ -558,7 +565,6 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
                 const bool need3 = sp.rule == 0 ? k2 > 0 : k2 < sp.Tnn;
                 if (need3) {
                     const uint8_t* src = smem + OFF_E + (b * NC + warp) * PATCH_BYTES;
-                    const uint8_t* lt = reinterpret_cast<const Prep*>(smem + OFF_PREP)[b * NC + warp].lut;
                     uint32_t* dst = reinterpret_cast<uint32_t*>(epatch + (int64_t)(c0 + warp) * kEPatchBytes);
                     for (int wi = lane; wi < kEPatchBytes / 4; wi += 32) {
                         uint32_t x = 0;
@@ -566,7 +572,7 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
                         for (int q = 0; q < 4; ++q) {
                             const int k = min(4 * wi + q, kPatchN - 1);
                             const int v = k / kPatchW, u = k - v * kPatchW;
-                            x |= (uint32_t)lt[src[v * EP + 4 + u]] << (8 * q);
+                            x |= (uint32_t)src[v * EP + 4 + u] << (8 * q);
                         }
                         dst[wi] = x;
                     }
