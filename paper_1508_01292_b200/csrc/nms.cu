@@ -11,9 +11,9 @@
 //
 // One CTA per frame, everything in shared memory: the frame's boxes are bitonic-sorted by
 // x so each box only tests the contiguous run of later boxes that start inside its width
-// (all-pairs was O(n^2) and instruction-bound on cluttered frames); lock-free union-find
+// (all-pairs was O(n^2) and instruction-bound on cluttered frames), a warp per box; lock-free union-find
 // (hook the larger root under the smaller, path splitting), shared-memory atomics for the
-// per-component sums, rank sort.  The last CTA to finish (ticket) compacts all frames'
+// per-component sums, rank sort in shared memory.  The last CTA to finish (ticket) compacts all frames'
 // results into one array.
 #include "ccnn_internal.h"
 
@@ -25,7 +25,7 @@ constexpr int kNmsThreads = 512;
 struct NmsSmem {
     short4 box[kNmsCap];         // x, y, w, h of this frame's raw boxes (sorted by x)
     float score[kNmsCap];
-    uint32_t key[kNmsCap];       // sort keys: x << 16 | arrival slot
+    uint32_t key[kNmsCap];       // sort keys: x << 16 | arrival slot (later: group sizes)
     int parent[kNmsCap];
     int sx[kNmsCap], sy[kNmsCap], sw[kNmsCap], sh[kNmsCap], cnt[kNmsCap];
     int best[kNmsCap];           // order-preserving int image of the max score
@@ -111,8 +111,8 @@ __global__ void __launch_bounds__(kNmsThreads) nms_kernel(
     }
     __syncthreads();
     const int n = sm.n;
-    // staging per frame: [0, kNmsCap) unsorted groups, [kNmsCap, 2 kNmsCap) sorted
-    OutBox* const st = staging + (int64_t)f * 2 * kNmsCap;
+    // staging per frame: kNmsCap slots for its sorted groups
+    OutBox* const st = staging + (int64_t)f * kNmsCap;
     if (n > kNmsCap) {
         if (tid == 0) { atomicExch(&ctrl->nms_overflow, 1u); frame_counts[f] = 0; }
     } else {
@@ -155,14 +155,24 @@ __global__ void __launch_bounds__(kNmsThreads) nms_kernel(
         }
         __syncthreads();
         // edges of the IoU >= 0.3 graph -> union-find; b > a with x_b >= x_a can only
-        // overlap a while x_b < x_a + w_a
-        for (int a = tid; a < n; a += kNmsThreads) {
-            const short4 ba = sm.box[a];
-            const int xend = ba.x + ba.z;
-            for (int b = a + 1; b < n; ++b) {
-                const short4 bb = sm.box[b];
-                if (bb.x >= xend) break;
-                if (iou_edge(ba, bb)) unite(sm.parent, a, b);
+        // overlap a while x_b < x_a + w_a.  A warp per box a, its lanes test 32 consecutive
+        // b at a time (the runs differ a lot in length on cluttered frames: one thread per a
+        // left the CTA waiting for its longest run)
+        {
+            const int lane = tid & 31;
+            for (int a = tid >> 5; a < n; a += kNmsThreads / 32) {
+                const short4 ba = sm.box[a];
+                const int xend = ba.x + ba.z;
+                for (int b0 = a + 1; b0 < n; b0 += 32) {
+                    const int b = b0 + lane;
+                    bool in = false;
+                    if (b < n) {
+                        const short4 bb = sm.box[b];
+                        in = bb.x < xend;
+                        if (in && iou_edge(ba, bb)) unite(sm.parent, a, b);
+                    }
+                    if (__ballot_sync(0xFFFFFFFFu, in) != 0xFFFFFFFFu) break;   // x-sorted: run ended
+                }
             }
         }
         __syncthreads();
@@ -177,26 +187,34 @@ __global__ void __launch_bounds__(kNmsThreads) nms_kernel(
             atomicMax(&sm.best[r], f2ord(sm.score[i]));
         }
         __syncthreads();
+        // the groups, compacted into the (no longer needed) box / score / key arrays: means
+        // fit in 16 bits (every coordinate does); key = the group's size
         for (int i = tid; i < n; i += kNmsThreads) {
             if (sm.parent[i] != i || sm.cnt[i] < min_cluster) continue;
             const int c = sm.cnt[i];
-            OutBox o;
-            o.frame = f;
-            o.x = (2 * sm.sx[i] + c) / (2 * c);
-            o.y = (2 * sm.sy[i] + c) / (2 * c);
-            o.w = (2 * sm.sw[i] + c) / (2 * c);
-            o.h = (2 * sm.sh[i] + c) / (2 * c);
-            o.score = ord2f(sm.best[i]);
-            o.neighbors = c;
-            st[atomicAdd(&sm.m, 1)] = o;
+            const int g = atomicAdd(&sm.m, 1);
+            sm.box[g] = make_short4((short)((2 * sm.sx[i] + c) / (2 * c)), (short)((2 * sm.sy[i] + c) / (2 * c)),
+                                    (short)((2 * sm.sw[i] + c) / (2 * c)), (short)((2 * sm.sh[i] + c) / (2 * c)));
+            sm.score[g] = ord2f(sm.best[i]);
+            sm.key[g] = (uint32_t)c;
         }
         __syncthreads();
         const int m = sm.m;
-        for (int i = tid; i < m; i += kNmsThreads) {             // rank sort
-            const OutBox a = st[i];
+        for (int i = tid; i < m; i += kNmsThreads) {             // rank sort (shared memory)
+            OutBox a;
+            a.frame = f;
+            a.x = sm.box[i].x; a.y = sm.box[i].y; a.w = sm.box[i].z; a.h = sm.box[i].w;
+            a.score = sm.score[i];
+            a.neighbors = (int)sm.key[i];
             int r = 0;
-            for (int j = 0; j < m; ++j) r += before(st[j], j, a, i);
-            st[kNmsCap + r] = a;
+            for (int j = 0; j < m; ++j) {
+                const short4 bj = sm.box[j];
+                OutBox b;
+                b.x = bj.x; b.y = bj.y; b.w = bj.z; b.h = bj.w;
+                b.score = sm.score[j];
+                r += before(b, j, a, i);
+            }
+            st[r] = a;
         }
         if (tid == 0) frame_counts[f] = m;
     }
@@ -246,7 +264,7 @@ __global__ void __launch_bounds__(kNmsThreads) nms_kernel(
             const int mid = (lo + hi + 1) >> 1;
             if (sm.sx[mid] <= i) lo = mid; else hi = mid - 1;
         }
-        out[i] = staging[(int64_t)lo * 2 * kNmsCap + kNmsCap + (i - sm.sx[lo])];
+        out[i] = staging[(int64_t)lo * kNmsCap + (i - sm.sx[lo])];
     }
     if (tid == 0) ctrl->n_out = (uint32_t)total;
 }

@@ -798,7 +798,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     CU(sl.resp2.ensure(sizeof(float) * 50 * (size_t)cand_cap));
     CU(sl.epatch.ensure((size_t)kEPatchBytes * cand_cap));
     CU(sl.acc.ensure(sizeof(AccBox) * cand_cap));
-    CU(sl.staging.ensure(sizeof(OutBox) * 2 * kNmsCap * (size_t)n));
+    CU(sl.staging.ensure(sizeof(OutBox) * kNmsCap * (size_t)n));
     CU(sl.counts.ensure(sizeof(int32_t) * n));
     CU(sl.out.ensure(sizeof(OutBox) * cand_cap));
     CU(sl.finfo.ensure(sizeof(FrameInfo) * n));
@@ -1247,7 +1247,7 @@ int ccnn_debug_group(ccnn_ctx* ctx, const ccnn_box* raw, int64_t n, int n_frames
     } guard{{&d_acc, &d_ctrl, &d_staging, &d_counts, &d_out}};
     CU(d_acc.ensure(sizeof(AccBox) * acc.size()));
     CU(d_ctrl.ensure(sizeof(Ctrl)));
-    CU(d_staging.ensure(sizeof(OutBox) * 2 * kNmsCap * (size_t)n_frames));
+    CU(d_staging.ensure(sizeof(OutBox) * kNmsCap * (size_t)n_frames));
     CU(d_counts.ensure(sizeof(int32_t) * n_frames));
     CU(d_out.ensure(sizeof(OutBox) * acc.size()));
     Ctrl hc{};
