@@ -8,7 +8,8 @@
 //
 // B200 design: a persistent kernel whose WARPS drain the survivor queue independently (one
 // atomic claim per survivor, no block barriers): K2 from resp2 by two ballots and the stop
-// decision; otherwise CNN3 on the equalised patch E that selective_tc.cu left in epatch, on the
+// decision (when there are no more survivors than CTAs -- small frames, latency -- a whole CTA
+// takes each survivor instead, the same code over 6 warps); otherwise CNN3 on the equalised patch E that selective_tc.cu left in epatch, on the
 // FFMA pipe (2-map layers: no dense contraction for the tensor cores), in the warp's own
 // shared-memory slice:
 //  * layer 1 (C4x4 1->2, pool, act), one orientation at a time: a lane computes 4 adjacent
@@ -53,18 +54,29 @@ __device__ __forceinline__ float act(float x)      // Eq. 1, see stage
     return copysignf(fmaf(-1.7159f, r, 1.7159f), x);
 }
 
-// CNN3 on both orientations of the warp's patch: lane l returns the responses of cells l and
-// l + 32 (cell c = orientation c / 25, position c % 25; -inf past 49)
-__device__ __forceinline__ void cnn3_warp(const Cnn3W& W, const float* __restrict__ w3s, WarpSmem& S,
-                                          float (&r)[2])
+// CNN3 on both orientations of the group's patch, by a group of G warps (G = 1: one warp per
+// survivor, the throughput form; G = kWarps: the whole CTA on one survivor, the latency form
+// used when there are no more survivors than CTAs).  gt = thread index in the group; thread gt
+// returns the responses of cells gt and gt + 32 G (cell c = orientation c / 25, position c % 25;
+// -inf past 49)
+template <int G>
+__device__ __forceinline__ void group_sync()
 {
-    const int lane = (int)(threadIdx.x & 31);
+    if constexpr (G == 1) __syncwarp();
+    else __syncthreads();
+}
+template <int G>
+__device__ __forceinline__ void cnn3_group(const Cnn3W& W, const float* __restrict__ w3s, WarpSmem& S,
+                                           int gt, float (&r)[2])
+{
+    constexpr int NG = 32 * G;
+    const int lane = gt & 31, wg = gt >> 5;
     const uint8_t* e = reinterpret_cast<const uint8_t*>(S.e);
 #pragma unroll 1
     for (int o = 0; o < 2; ++o) {
         // ---- layer 1: item = (pooled row py, pooled columns 4q .. 4q+3): 26 x 6 items ----
 #pragma unroll 1
-        for (int it = lane; it < 26 * 6; it += 32) {
+        for (int it = gt; it < 26 * 6; it += NG) {
             const int py = it / 6, q = it - py * 6;
             // image column 8q + c is E column x0 + dx * c: M(x) = E(50 - x) for o = 1 (one code
             // path for both orientations keeps the kernel's instruction footprint small)
@@ -93,10 +105,10 @@ __device__ __forceinline__ void cnn3_warp(const Cnn3W& W, const float* __restric
                     S.p1[a][py][4 * q + j] = act(fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3])));  // pool, act
                 }
         }
-        __syncwarp();
+        group_sync<G>();
         // ---- layer 2: item = pooled position (12 rows x 11 columns) ----
 #pragma unroll 1
-        for (int it = lane; it < 12 * 11; it += 32) {
+        for (int it = gt; it < 12 * 11; it += NG) {
             const int py = it / 11, px = it - py * 11;
             float s2[2][4];
 #pragma unroll
@@ -124,11 +136,12 @@ __device__ __forceinline__ void cnn3_warp(const Cnn3W& W, const float* __restric
             for (int b = 0; b < 2; ++b)
                 S.p2[o][b][py][px] = act(fmaxf(fmaxf(s2[b][0], s2[b][1]), fmaxf(s2[b][2], s2[b][3])));
         }
-        __syncwarp();                               // P2 complete; P1 free for the next orientation
+        group_sync<G>();                            // P2 complete; P1 free for the next orientation
     }
     // ---- layer 3: a lane per map m (lanes 25-31 idle), one input channel at a time with its
     //      7 x 8 kernel in registers; a pass walks the 10 response rows (orientation, y), the
-    //      P2 rows broadcast to the warp as float4s; channel 0 leaves partial sums in l3 ----
+    //      P2 rows broadcast to the warp as float4s; channel 0 leaves partial sums in l3; the
+    //      group's warps split the response rows ----
     float* l3 = S.l3;                               // [m][kL3S] (P1 is dead by now)
     const int m = lane < 25 ? lane : 24;
 #pragma unroll 1
@@ -138,7 +151,7 @@ __device__ __forceinline__ void cnn3_warp(const Cnn3W& W, const float* __restric
         for (int k = 0; k < 56; ++k) w[k] = w3s[m * kW3S + ch * 56 + k];
         const float b = w3s[m * kW3S + 112];
 #pragma unroll 1
-        for (int oy = 0; oy < 10; ++oy) {
+        for (int oy = wg; oy < 10; oy += G) {
             const int o = oy / 5, y = oy - o * 5;
             float a[5];
 #pragma unroll
@@ -159,11 +172,11 @@ __device__ __forceinline__ void cnn3_warp(const Cnn3W& W, const float* __restric
             }
         }
     }
-    __syncwarp();
-    // ---- layer 4 (C1x1 25->1, act): a lane per response cell (lanes 0-17 take two) ----
+    group_sync<G>();
+    // ---- layer 4 (C1x1 25->1, act): a thread per response cell ----
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        const int c = lane + 32 * h;
+        const int c = gt + NG * h;
         float rr = W.b4;
         if (c < 2 * kResp) {
 #pragma unroll
@@ -171,7 +184,7 @@ __device__ __forceinline__ void cnn3_warp(const Cnn3W& W, const float* __restric
         }
         r[h] = c < 2 * kResp ? act(rr) : -INFINITY;
     }
-    __syncwarp();                                   // l3 / P1 reused by the next survivor
+    group_sync<G>();                                // l3 / P1 reused by the next survivor
 }
 
 __global__ void __launch_bounds__(32 * kWarps, 3) selective_kernel(
@@ -195,6 +208,73 @@ __global__ void __launch_bounds__(32 * kWarps, 3) selective_kernel(
         for (int d = 16; d >= 1; d >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, d));
         return v;
     };
+    // the survivor's outcome (one thread): SelOut, Table-1 counters, the accepted-box list
+    auto finish = [&](int ci, int K2, int K3, int delta, int ran3, float best) {
+        const S1Cand cd = cands[ci];
+        SelOut so;
+        so.K2 = K2; so.K3 = K3; so.delta = delta; so.cnn3_ran = ran3; so.score = best;
+        sel::raw_box(cd, lvinfo[cd.level].sigma, so);              // O8
+        out[ci] = so;
+        if (K2 > 0) atomicAdd(&ctrl->n_stage2, 1u);
+        if (delta) {
+            atomicAdd(&ctrl->n_stage3, 1u);
+            const uint32_t k = atomicAdd(&ctrl->n_acc, 1u);
+            AccBox b;
+            b.frame = cd.frame; b.x = so.bx; b.y = so.by; b.w = so.bw; b.h = so.bh; b.score = best;
+            acc[k] = b;                   // n_acc <= n_cand <= cand_cap slots
+        }
+    };
+    if (n_cand <= gridDim.x) {
+        // ---- latency form: no more survivors than CTAs -> a whole CTA per survivor ----
+        __shared__ int s_ci;
+        __shared__ float s_wmax[kWarps];
+        WarpSmem& S0 = reinterpret_cast<WarpSmem*>(sraw + kW3Bytes)[0];
+        const int tid = (int)threadIdx.x;
+        auto block_max = [&](float v) {
+            v = warp_max(v);
+            if (lane == 0) s_wmax[tid >> 5] = v;
+            __syncthreads();
+            float m = s_wmax[0];
+#pragma unroll
+            for (int k = 1; k < kWarps; ++k) m = fmaxf(m, s_wmax[k]);
+            __syncthreads();
+            return m;
+        };
+        for (;;) {
+            if (tid == 0) s_ci = (int)atomicAdd(&ctrl->sel_next, 1u);
+            __syncthreads();
+            const int ci = s_ci;
+            if ((uint32_t)ci >= n_cand) break;                  // CTA-uniform
+            const float r2v = tid < 2 * kResp ? resp2[(int64_t)ci * 50 + tid] : -INFINITY;
+            const int K2 = __syncthreads_count(r2v > sp.T2a);
+            const bool stop = (sp.rule == 0) ? (K2 == 0) : (K2 >= sp.Tnn);
+            int K3 = 0, delta, ran3 = 0;
+            float best, r3[2] = {0.f, 0.f};
+            if (stop) {
+                delta = (sp.rule == 0) ? 0 : 1;
+                best = block_max(r2v);
+            } else {
+                const uint4* src = reinterpret_cast<const uint4*>(epatch + (int64_t)ci * kEPatchBytes);
+                uint4* dst = reinterpret_cast<uint4*>(S0.e);
+                for (int w = tid; w < kEPatchBytes / 16; w += 32 * kWarps) dst[w] = __ldg(src + w);
+                __syncthreads();
+                cnn3_group<kWarps>(W3, w3s, S0, tid, r3);          // cells tid (< 50) only
+                K3 = __syncthreads_count(r3[0] > sp.T2b);
+                ran3 = 1;
+                delta = (sp.rule == 0) ? (((K2 >= sp.Tnn) && K3 > 0) || (K2 > 0 && K3 >= sp.Tnn))
+                                       : (K2 >= sp.Tnn || K3 >= sp.Tnn);
+                best = block_max(r3[0]);
+            }
+            if (dbg_resp && tid < 2 * kResp) {
+                dbg_resp[(int64_t)ci * 100 + tid] = r2v;
+                dbg_resp[(int64_t)ci * 100 + 50 + tid] = r3[0];
+            }
+            if (tid == 0) finish(ci, K2, K3, delta, ran3, best);
+            __syncthreads();                                    // s_ci / S0 reused
+        }
+        return;
+    }
+    // ---- throughput form: one warp per survivor ----
     for (;;) {
         int ci = 0;
         if (lane == 0) ci = (int)atomicAdd(&ctrl->sel_next, 1u);
@@ -219,7 +299,7 @@ __global__ void __launch_bounds__(32 * kWarps, 3) selective_kernel(
             for (int w = lane; w < kEPatchBytes / 16; w += 32) dst[w] = __ldg(src + w);
             __syncwarp();
             // ---- CNN3 on both orientations, K3, the rule (P:95 / P:217) ----
-            cnn3_warp(W3, w3s, S, r3);
+            cnn3_group<1>(W3, w3s, S, lane, r3);
             K3 = __popc(__ballot_sync(0xFFFFFFFFu, r3[0] > sp.T2b)) +
                  __popc(__ballot_sync(0xFFFFFFFFu, r3[1] > sp.T2b));
             ran3 = 1;
@@ -237,21 +317,7 @@ __global__ void __launch_bounds__(32 * kWarps, 3) selective_kernel(
                 d[50 + lane + 32] = r3[1];
             }
         }
-        if (lane == 0) {
-            const S1Cand cd = cands[ci];
-            SelOut so;
-            so.K2 = K2; so.K3 = K3; so.delta = delta; so.cnn3_ran = ran3; so.score = best;
-            sel::raw_box(cd, lvinfo[cd.level].sigma, so);              // O8
-            out[ci] = so;
-            if (K2 > 0) atomicAdd(&ctrl->n_stage2, 1u);
-            if (delta) {
-                atomicAdd(&ctrl->n_stage3, 1u);
-                const uint32_t k = atomicAdd(&ctrl->n_acc, 1u);
-                AccBox b;
-                b.frame = cd.frame; b.x = so.bx; b.y = so.by; b.w = so.bw; b.h = so.bh; b.score = best;
-                acc[k] = b;               // n_acc <= n_cand <= cand_cap slots
-            }
-        }
+        if (lane == 0) finish(ci, K2, K3, delta, ran3, best);
     }
 }
 
