@@ -948,9 +948,13 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
         CU(cudaEventCreate(&ctx->epoch));
         CU(cudaEventRecord(ctx->epoch, ps));
     }
-    sl.pyr_launches = launch_pyramid(dfi, n, ctx->pyr_tiles, ctx->pyr_class_max, ctx->all_safe, use_tex,
-                                     sl.arena.as<uint8_t>(), ctx->d_levels.as<LevelInfo>(),
-                                     ctx->d_ptiles.as<uint32_t>(), ctx->d_tabs.as<uint32_t>(), ps);
+    // CCNN_EXP_SKIP_PYRAMID=1 (timing experiments only, results invalid unless every batch
+    // repeats the slot's previous frames): no pyramid launch, stage 1 reads the slot's old levels
+    static const bool exp_skip_pyr = std::getenv("CCNN_EXP_SKIP_PYRAMID") != nullptr;
+    sl.pyr_launches = (exp_skip_pyr && sl.used) ? 0 :
+        launch_pyramid(dfi, n, ctx->pyr_tiles, ctx->pyr_class_max, ctx->all_safe, use_tex,
+                       sl.arena.as<uint8_t>(), ctx->d_levels.as<LevelInfo>(),
+                       ctx->d_ptiles.as<uint32_t>(), ctx->d_tabs.as<uint32_t>(), ps);
     CU(cudaEventRecord(sl.ev[3], ps));
     // stage 1 on the compute stream once the slot's previous batch has finished with the
     // slot's queue / scratch (its tail) and this batch's pyramid is done

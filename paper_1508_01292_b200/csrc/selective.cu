@@ -8,8 +8,8 @@
 //
 // B200 design: a persistent kernel whose WARPS drain the survivor queue independently (one
 // atomic claim per survivor, no block barriers): K2 from resp2 by two ballots and the stop
-// decision (when there are no more survivors than CTAs -- small frames, latency -- a whole CTA
-// takes each survivor instead, the same code over 6 warps); otherwise CNN3 on the equalised patch E that selective_tc.cu left in epatch, on the
+// decision (with few survivors -- at most 4 per CTA: small frames, sparse 4K -- a whole CTA
+// takes each survivor instead, the same code over 6 warps: latency); otherwise CNN3 on the equalised patch E that selective_tc.cu left in epatch, on the
 // FFMA pipe (2-map layers: no dense contraction for the tensor cores), in the warp's own
 // shared-memory slice:
 //  * layer 1 (C4x4 1->2, pool, act), one orientation at a time: a lane computes 4 adjacent
@@ -21,6 +21,8 @@
 //    rows broadcast as float4s -- 0.1 shared loads per FMA, no constant-cache traffic;
 //  * layer 4 (C1x1 25->1, act): a lane per response cell.
 // CNN3 = architecture R (R1): C4x4 1->2, P, C3x3 2->2, P, C7x8 2->25, C1x1 25->1.
+#include <cstdlib>
+
 #include "ccnn_internal.h"
 #include "selective_common.cuh"
 
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(32 * kWarps, 3) selective_kernel(
     const __grid_constant__ Cnn3W W3, const SelParams sp, const LevelInfo* __restrict__ lvinfo,
     const S1Cand* __restrict__ cands, const uint32_t cand_cap, const float* __restrict__ resp2,
     const uint8_t* __restrict__ epatch, SelOut* __restrict__ out, float* __restrict__ dbg_resp,
-    AccBox* __restrict__ acc, Ctrl* __restrict__ ctrl)
+    AccBox* __restrict__ acc, Ctrl* __restrict__ ctrl, const uint32_t cta_max)
 {
     extern __shared__ __align__(16) unsigned char sraw[];
     const int lane = (int)(threadIdx.x & 31);
@@ -224,8 +226,8 @@ __global__ void __launch_bounds__(32 * kWarps, 3) selective_kernel(
             acc[k] = b;                   // n_acc <= n_cand <= cand_cap slots
         }
     };
-    if (n_cand <= gridDim.x) {
-        // ---- latency form: no more survivors than CTAs -> a whole CTA per survivor ----
+    if (n_cand <= cta_max) {
+        // ---- latency form (few survivors): a whole CTA per survivor ----
         __shared__ int s_ci;
         __shared__ float s_wmax[kWarps];
         WarpSmem& S0 = reinterpret_cast<WarpSmem*>(sraw + kW3Bytes)[0];
@@ -333,8 +335,17 @@ void launch_selective(const Cnn3W& w3, SelParams sp, const LevelInfo* d_levels,
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, selective_kernel, 32 * kWarps, smem);
     if (occ < 1) occ = 1;
-    selective_kernel<<<sm_count * occ, 32 * kWarps, smem, s>>>(w3, sp, d_levels, cands, cand_cap, resp2,
-                                                              epatch, out, dbg_resp, acc, ctrl);
+    // a lone warp needs ~40 us for one survivor's CNN3, a CTA ~10 us: below a few survivors
+    // per CTA the CTA form finishes first (C4: 700 survivors -> 73 -> ~25 us), above it the
+    // warp form's throughput wins (C5: 45k survivors)
+    static const long env_max = [] {
+        const char* e = std::getenv("CCNN_CNN3_CTA_PER_GRID");     // experiments only
+        return e ? std::atol(e) : -1L;
+    }();
+    const int grid = sm_count * occ;
+    const uint32_t cta_max = (uint32_t)(env_max >= 0 ? env_max * grid : 4L * grid);
+    selective_kernel<<<grid, 32 * kWarps, smem, s>>>(w3, sp, d_levels, cands, cand_cap, resp2,
+                                                     epatch, out, dbg_resp, acc, ctrl, cta_max);
 }
 
 }  // namespace ccnn
