@@ -829,22 +829,34 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     GrayJob* jobs = sl.h_jobs;
     int n_jobs = 0;
     {
-        // device copies (host gray frames, and every RGB frame's gray plane): pitch and frame
-        // offsets meet the texture alignment; host RGB frames are staged as they come
+        // device copies: host gray frames keep the caller's pitch and a run of equally-sized
+        // frames lying back to back in host memory stays back to back (one linear H2D for the
+        // run: a pitched 2-D copy of short rows runs far below the PCIe rate); every RGB frame's
+        // gray plane, and every frame when the texture pyramid is requested, gets a pitch and
+        // frame offset that meet the texture alignment; host RGB frames are staged as they come
         const int64_t pa = std::max<int64_t>(16, ctx->tex_pitch_align);
         const int64_t fa = std::max<int64_t>(256, ctx->tex_align);
+        const bool tex_layout = (ctx->debug & CCNN_DEBUG_PYR_TEX) != 0;
         auto chans = [&](int f) { return frames[f].channels == 0 ? 1 : frames[f].channels; };
-        std::vector<int64_t> foff(n, -1), roff(n, -1);
+        std::vector<int64_t> foff(n, -1), roff(n, -1), dpv(n, 0);
         int64_t total = 0, rtotal = 0;
         for (int f = 0; f < n; ++f) {
             if (frames_on_device && chans(f) == 1) continue;      // used in place
+            const bool keep = !tex_layout && chans(f) == 1;      // host gray frame
+            dpv[f] = keep ? frames[f].pitch : round_up(frames[f].w, pa);
+            const bool follows = keep && f > 0 && foff[f - 1] >= 0 && chans(f - 1) == 1 &&
+                                 dpv[f - 1] == dpv[f] && frames[f - 1].w == frames[f].w &&
+                                 frames[f - 1].h == frames[f].h &&
+                                 frames[f].data == frames[f - 1].data + dpv[f] * frames[f].h;
+            if (!follows) total = round_up(total, fa);
             foff[f] = total;
-            total += round_up(round_up(frames[f].w, pa) * (int64_t)frames[f].h, fa);
+            total += dpv[f] * (int64_t)frames[f].h;
             if (!frames_on_device && chans(f) == 3) {
                 roff[f] = rtotal;
                 rtotal += round_up(round_up(3LL * frames[f].w, 16) * frames[f].h, 256);
             }
         }
+        total = round_up(total, fa);
         if (total) {
             const void* old_p = sl.frames.p;
             const size_t old_bytes = sl.frames.bytes;
@@ -859,7 +871,7 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
                 fi[f] = FrameInfo{frames[f].data, frames[f].pitch, frames[f].w, frames[f].h};
                 continue;
             }
-            const int64_t dp = round_up(frames[f].w, pa);
+            const int64_t dp = dpv[f];
             fi[f] = FrameInfo{gbuf + foff[f], dp, frames[f].w, frames[f].h};
             if (chans(f) == 3) {
                 const bool staged = !frames_on_device;
@@ -888,16 +900,22 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
                     ++f;
                     continue;
                 }
-                // one 2-D copy for every run of equally-sized gray frames laid out back to back
+                // one copy for every run of equally-sized gray frames laid out back to back (in
+                // host memory and, by the layout above, in the slot buffer)
                 int g = f + 1;
-                const int64_t dp = round_up(frames[f].w, pa);
+                const int64_t dp = dpv[f];
                 while (g < n && chans(g) == 1 && frames[g].w == frames[f].w &&
                        frames[g].h == frames[f].h && frames[g].pitch == frames[f].pitch &&
                        frames[g].data == frames[f].data + (int64_t)(g - f) * frames[f].h * frames[f].pitch &&
                        foff[g] == foff[f] + (int64_t)(g - f) * dp * frames[f].h)
                     ++g;
-                CU(cudaMemcpy2DAsync(gbuf + foff[f], dp, frames[f].data, frames[f].pitch, frames[f].w,
-                                     (size_t)frames[f].h * (g - f), cudaMemcpyHostToDevice, cs));
+                const int64_t rows = (int64_t)frames[f].h * (g - f);
+                if (dp == frames[f].pitch)             // linear: up to the run's last pixel
+                    CU(cudaMemcpyAsync(gbuf + foff[f], frames[f].data, (size_t)(dp * (rows - 1) + frames[f].w),
+                                       cudaMemcpyHostToDevice, cs));
+                else
+                    CU(cudaMemcpy2DAsync(gbuf + foff[f], dp, frames[f].data, frames[f].pitch, frames[f].w,
+                                         (size_t)rows, cudaMemcpyHostToDevice, cs));
                 f = g;
             }
         }
