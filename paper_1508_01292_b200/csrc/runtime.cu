@@ -996,6 +996,9 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     cudaStream_t ts = ctx->tail;
     CU(cudaStreamWaitEvent(ts, sl.ev[4], 0));
     CU(cudaEventRecord(sl.ev[8], ts));
+    // CCNN_EXP_SKIP_TAIL=1 (timing experiments only, results invalid): no selective unit / NMS
+    static const bool exp_skip_tail = std::getenv("CCNN_EXP_SKIP_TAIL") != nullptr;
+    if (!exp_skip_tail) {
     launch_selective_cnn2_tc(ctx->sel_consts, ctx->sp, ctx->sel_bmats.as<uint16_t>(), dfi,
                              ctx->d_levels.as<LevelInfo>(), sl.cands.as<S1Cand>(), cand_cap,
                              sl.resp2.as<float>(), sl.epatch.as<uint8_t>(), dctrl,
@@ -1007,6 +1010,9 @@ int ccnn_submit_frames(ccnn_ctx* ctx, const ccnn_frame* frames, int n, int frame
     CU(cudaEventRecord(sl.ev[5], ts));
     launch_nms(sl.acc.as<AccBox>(), dctrl, n, ctx->min_cluster, sl.staging.as<OutBox>(),
                sl.counts.as<int32_t>(), sl.out.as<OutBox>(), ts);
+    } else {
+        CU(cudaEventRecord(sl.ev[5], ts));
+    }
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(sl.h_ctrl, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, ts));
     CU(cudaEventRecord(sl.ev[6], ts));

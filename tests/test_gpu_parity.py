@@ -348,6 +348,33 @@ def test_host_vs_device_frames_and_determinism(ws):
     big[:, :, :c.width] = dev
     f = det.detect(big[:, :, :c.width], c.min_face, c.scale_step)
     assert np.array_equal(a, f)
+    # pitched host batches (odd pitch; pageable and pinned): the slot buffer keeps the caller's
+    # pitch and the batch lands with one linear copy
+    hb = torch.zeros((4, c.height, c.width + 37), dtype=torch.uint8)
+    hb[:, :, :c.width] = torch.from_numpy(fr)
+    assert np.array_equal(a, det.detect(hb[:, :, :c.width], c.min_face, c.scale_step))
+    assert np.array_equal(a, det.detect(hb.pin_memory()[:, :, :c.width], c.min_face, c.scale_step))
+
+
+def test_host_frames_odd_width_linear_copy(ws, cascade):
+    """C2-like stills of odd width (450: rows not 16-B aligned) from host memory, contiguous
+    (one linear H2D of the whole batch, device pitch 450) and pinned, equal the device-resident
+    detection and the oracle's levels."""
+    import torch
+    from paper_1508_01292_b200 import ccnn
+    fr = synth_frames.make_stills(6, 450, 451, 77, 15)
+    T1, T2 = configs.C2.thresholds()
+    det = make_det(ws, T1, T2, configs.C2.Tnn, configs.C2.rule, max_w=450, max_h=451, max_batch=8)
+    ref = det.detect(torch.from_numpy(fr).cuda(), 15, 1.05)
+    det.set_debug(ccnn.CCNN_DEBUG_LEVELS)
+    assert np.array_equal(det.detect(fr, 15, 1.05), ref)
+    lv = oracle.level_table(450, 451, 15, 1.05)
+    for f in (0, 5):
+        for l in (0, len(lv) // 2, len(lv) - 1):
+            s, lw, lh = lv[l]
+            assert np.array_equal(det.level_image(f, l), oracle.resample(fr[f], s, lw, lh))
+    assert np.array_equal(det.detect(torch.from_numpy(fr).pin_memory(), 15, 1.05), ref)
+    assert len(ref) > 0
 
 
 def test_streaming_submit_collect(ws):
