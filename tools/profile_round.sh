@@ -25,7 +25,7 @@ if has launches; then
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -s 20 -c 12 --csv --log-file gpurun_out/launches_c4_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-traffic --e2e-steps 1 > /dev/null 2>&1
 fi
 if has ncu; then
-  for k in stage1_tc pyramid_gather4 selective_cnn2 selective_kernel nms; do
+  for k in ${NCU_KERNELS:-stage1_tc pyramid_gather4 selective_cnn2 selective_kernel nms}; do
     timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 -o gpurun_out/prof_${k}_$TAG python tools/stage_times.py c4 2 > gpurun_out/ncu_${k}_$TAG.log 2>&1
   done
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:selective_cnn2 -s 1 -c 1 -o gpurun_out/prof_cnn2_c5_$TAG python tools/stage_times.py c5 1 > gpurun_out/ncu_cnn2_c5_$TAG.log 2>&1
