@@ -1,7 +1,8 @@
 // tc05.cuh -- thin sm_100a wrappers (inline PTX) for the 5th-generation tensor cores:
 // TMEM allocation, tcgen05.mma (kind::f16, operands in shared memory), commit to an mbarrier,
 // tcgen05.ld of accumulators, and the shared-memory matrix / instruction descriptors.
-// Used by stage1_tc.cu (layers 1-3 of CNN1 as implicit-GEMM convolutions).  Not ABI.
+// Used by stage1_tc.cu (CNN1 layers 1-3) and selective_tc.cu (CNN2 layers 1-3) as implicit-GEMM
+// convolutions.  Not ABI.
 //
 // Shared-memory matrix descriptor (no swizzle, K-major "interleaved" canonical layout): the
 // operand is a grid of 8-row x 16-byte core matrices, each core matrix 128 contiguous bytes
