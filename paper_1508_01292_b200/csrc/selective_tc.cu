@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ int s_claim, s_strip[2], s_nc[2], s_k2[2][NC];
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) uint64_t bar_l1, bar_l2, bar_l3, bar_full[2], bar_empty[2];
+    __shared__ __align__(8) uint64_t bar_l1, bar_l1a, bar_l2, bar_l3, bar_full[2], bar_empty[2];
 
     const int tid = threadIdx.x;
     const int warp = __shfl_sync(0xFFFFFFFFu, tid >> 5, 0);   // provably warp-uniform
@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
     if (mma_warp) tc05::tmem_alloc(&s_tmem, TM_COLS);
     if (tid == 0) {
         tc05::mbar_init(&bar_l1, 1);
+        tc05::mbar_init(&bar_l1a, 1);
         tc05::mbar_init(&bar_l2, 1);
         tc05::mbar_init(&bar_l3, 1);
         for (int b = 0; b < 2; ++b) {
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
     __syncthreads();
     tc05::fence_after();
     const uint32_t tm = s_tmem;
-    uint32_t ph_l1 = 0, ph_l2 = 0, ph_l3 = 0;     // completed phases (waiting side's count)
+    uint32_t ph_l1 = 0, ph_l1a = 0, ph_l2 = 0, ph_l3 = 0;   // completed phases (waiting side's count)
     const uint32_t s_base = tc05::smem_u32(smem);
 
     const int qd = warp & 3, hf = (warp >> 2) & 1;
@@ -397,9 +398,13 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
             };
             // layer-1 epilogue of unit k, maps 8 hf .. 8 hf + 7: P1 rows 2k + rr, columns 2X + cx
             // -> k chunk hf of the P1 entries; accumulator column h*64 + cx*32 + pos*8 + j
+            // waits for P1 row rr's MMAs (committed apart: bar_l1a row 0, bar_l1 both rows)
             auto l1_epilogue = [&](int k) {
 #pragma unroll 1
                 for (int rr = 0; rr < 2; ++rr) {
+                    if (rr == 0) { tc05::mbar_wait(&bar_l1a, ph_l1a & 1); ++ph_l1a; }
+                    else { tc05::mbar_wait(&bar_l1, ph_l1 & 1); ++ph_l1; }
+                    tc05::fence_after();
                     const int slot1 = (2 * k + rr) % P1_RING;
 #pragma unroll 1
                     for (int cx = 0; cx < 2; ++cx) {
@@ -490,10 +495,6 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
                 tc05::fence_before();
                 tc05::named_sync(BAR_PIPE, NPIPE);
             };
-            auto wait_l1 = [&]() {
-                tc05::mbar_wait(&bar_l1, ph_l1 & 1); ++ph_l1;
-                tc05::fence_after();
-            };
 
             // K2 counters of this buffer (last read two strips ago, before the previous strip's syncs)
             if (warp == 4 && lane < NC) s_k2[b][lane] = 0;
@@ -511,7 +512,6 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
                 uint32_t wx[2][2];
 #pragma unroll
                 for (int i = 0; i < 2; ++i) fetch(8 + 2 * i + hf, wx[i]);
-                wait_l1();
                 l1_epilogue(0);
                 if (hf == 0) {
                     st_zero24(tm + t_lane + TM_D2);
@@ -532,14 +532,14 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
 #pragma unroll
                     for (int i = 0; i < 2; ++i) fetch(4 * q + 12 + 2 * i + hf, wx[i]);
                 }
+                // the MMAs run in the order L1(q+1) [P1 row 0, then row 1], L2s(q), L3(q-2): the
+                // largest epilogue (layer 1, all data warps) starts first, P1 row by P1 row, and
+                // only the short layer-3 epilogue trails the last MMA
+                if (q + 1 <= NQ) l1_epilogue(q + 1);
                 if (q >= 2 && hf == 1) {
                     tc05::mbar_wait(&bar_l3, ph_l3 & 1); ++ph_l3;      // L3(q-2) done
                     tc05::fence_after();
                     l3_epilogue(q - 2);
-                }
-                if (q + 1 <= NQ) {
-                    wait_l1();
-                    l1_epilogue(q + 1);
                 }
                 if (q <= NQ && hf == 0) {
                     tc05::mbar_wait(&bar_l2, ph_l2 & 1); ++ph_l2;      // L2s(q) done
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
                     for (int i = 0; i < 2; ++i) put(4 * q + 12 + 2 * i + hf, wx[i]);
                 }
                 tc05::st_wait();
-                sync_for_mma();                                // -> L3(q-1), L1(q+2), L2s(q+1)
+                sync_for_mma();                                // -> L1(q+2), L2s(q+1), L3(q-1)
             }
             // the equalised patches of the survivors the rule sends to CNN3 (K2 > 0 under Eq. 2,
             // K2 < T_nn under Eq. 3; P:99 / S:358) -> epatch, for selective.cu
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
             auto issue_l1 = [&](int k) {
                 if (tc05::elect_one()) {
 #pragma unroll
-                    for (int rr = 0; rr < 2; ++rr)
+                    for (int rr = 0; rr < 2; ++rr) {
 #pragma unroll
                         for (int t = 0; t < 3; ++t)
 #pragma unroll
@@ -602,6 +602,8 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
                                                  bd1 + (uint64_t)(((t * 2 + hl) * B1M) >> 4), IDESC1,
                                                  (t | hl) != 0);
                             }
+                        if (rr == 0) tc05::commit(&bar_l1a);
+                    }
                     tc05::commit(&bar_l1);
                 }
                 __syncwarp();
@@ -650,9 +652,9 @@ __global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
             for (int q = 0; q <= NQ + 1; ++q) {
                 tc05::named_sync(BAR_PIPE, NPIPE);
                 tc05::fence_after();
-                if (q >= 1 && q <= NQ) issue_l3(q - 1);
                 if (q + 2 <= NQ) issue_l1(q + 2);
                 if (q + 1 <= NQ) issue_l2s(q + 1);
+                if (q >= 1 && q <= NQ) issue_l3(q - 1);
             }
         }
     }
