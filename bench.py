@@ -43,6 +43,19 @@ def stage1_alg_flops(levels):
     return tot
 
 
+def split_mma_factor(levels):
+    """MMAs per fp32-accurate product in stage 1, weighted by the layers' algorithmic FLOPs:
+    layer 1 multiplies exact fp16 pixels by hi + lo weights (2 MMAs), layers 2-3 split both
+    operands (hi*hi + hi*lo + lo*hi: 3 MMAs); layer 4 (1x1) runs on the FFMA pipe and counts
+    at 3 like its layer-3 neighbour (it is 0.5% of the work)."""
+    l1 = l23 = 0
+    for _, lw, lh in levels:
+        nx, ny = (lw - 27) // 4 + 1, (lh - 31) // 4 + 1
+        l1 += (4 * nx + 20) * (4 * ny + 24) * 6 * 16
+        l23 += (2 * nx + 8) * (2 * ny + 10) * 6 * 54 + nx * ny * (2 * 180 + 2)
+    return (2.0 * l1 + 3.0 * l23) / (l1 + l23) if l1 + l23 else 3.0
+
+
 def level_table(W, H, min_face, sf):
     """Level sizes for reporting (same O1 rule as the library; floats only for counting)."""
     out = []
@@ -569,6 +582,12 @@ def main():
                                       "zero taps; DESIGN.md K2)",
                          "fp32_ffma_peak": fp32_peak,
                          "frac_of_fp32_ffma_peak": achieved_tflops / fp32_peak,
+                         # fp32 accuracy costs 2 (layer 1) or 3 (layers 2-3) fp16 MMAs per
+                         # product: the fp16 peak divided by that FLOP-weighted factor is the
+                         # most fp32-accurate work the tensor cores can do (K2)
+                         "fp32_split_mmas_per_product": split_mma_factor(levels),
+                         "fp32_split_peak": tc_peak / split_mma_factor(levels),
+                         "frac_of_fp32_split_peak": achieved_tflops * split_mma_factor(levels) / tc_peak,
                          # the tensor work the kernel actually issues (all MMAs, zero taps and
                          # hi/lo splits included) over the same time: how busy the tensor
                          # cores are, as opposed to how much of it the algorithm needs

@@ -47,3 +47,17 @@ def test_stage1_alg_flops_brute_force_small():
 def test_parse_cpulist():
     assert bench.parse_cpulist("0-3,8,10-11\n") == {0, 1, 2, 3, 8, 10, 11}
     assert bench.parse_cpulist("") == set()
+
+
+def test_split_mma_factor_between_2_and_3():
+    """FLOP-weighted MMAs per fp32-accurate product: 2 for layer 1 (exact pixels x hi+lo
+    weights), 3 for layers 2-4; the C4 pyramid's weighting equals the per-layer closed form."""
+    lv = bench.level_table(3840, 2160, 60, 1.2)
+    f = bench.split_mma_factor(lv)
+    l1 = l23 = 0
+    for _, w, h in lv:
+        nx, ny = (w - 27) // 4 + 1, (h - 31) // 4 + 1
+        l1 += (4 * nx + 20) * (4 * ny + 24) * 96
+        l23 += (2 * nx + 8) * (2 * ny + 10) * 324 + nx * ny * 362
+    assert abs(f - (2 * l1 + 3 * l23) / (l1 + l23)) < 1e-12
+    assert 2.0 < f < 3.0 and abs(f - 2.513) < 5e-3       # layer 1 is ~49% of the FLOPs
