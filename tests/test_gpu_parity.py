@@ -52,6 +52,21 @@ def test_c1_parity_calibrated(ws, cascade):
     print(rep)
 
 
+@pytest.mark.parametrize("sf", [1.05, 1.1, 1.2])
+def test_c1_parity_scale_sweep(ws, cascade, sf):
+    """SURVEY §8(c) coverage plan: C1 at scale_step 1.05 / 1.1 / 1.2 (45 / 23 / 12 levels incl.
+    the upscaled ones) with T1 at the 1e-2 survival quantile; thresholds placed with a margin on
+    the frame, so maps, survivors, K2/K3/delta, every box and the Table-1 counts are exact."""
+    c = configs.C1
+    fr = c.make_frames()
+    T1, T2 = exact(cascade, fr, c.min_face, sf, 0.99, rule=c.rule, Tnn=c.Tnn)
+    det = make_det(ws, T1, T2, c.Tnn, c.rule)
+    rep = parity.compare_run(det, cascade, fr, c.min_face, sf, T1, T2, c.Tnn, c.rule,
+                             expect_exact=True)
+    assert rep["frames_boxes_checked"] == 1 and rep["survivors"] > 100 and rep["boxes"] > 0
+    print(sf, rep)
+
+
 @pytest.mark.parametrize("rule", [0, 1])
 def test_c1_parity_low_threshold(ws, cascade, rule):
     """T1 near the 97% quantile so ~400 windows reach the selective unit; thresholds with a
