@@ -344,6 +344,35 @@ def test_edge_cases(ws, cascade):
     assert e.value.code == ccnn.CCNN_E_CAPACITY
 
 
+def test_8k_frame_max_size(ws, cascade):
+    """A frame twice the 4K size in each dimension (7680 x 4320, min face 60: level 0 3456 x 1944,
+    23 levels, 1.27 M windows): dense stage-1 maps, survivors, selective outcomes, every box and
+    the Table-1 counts against the oracle, thresholds placed with a margin on the frame."""
+    fr = synth_frames.make_still(7680, 4320, 8080, 60)[None]
+    T1, T2 = exact(cascade, fr, 60, 1.2, 1.0 - 2e-4, Tnn=2)
+    det = make_det(ws, T1, T2, 2, 0, max_w=7680, max_h=4320, max_batch=1)
+    rep = parity.compare_run(det, cascade, fr, 60, 1.2, T1, T2, 2, 0, expect_exact=True)
+    assert rep["frames_boxes_checked"] == 1 and rep["survivors"] > 50
+    print(rep)
+
+
+def test_large_batch_equals_32_frame_batches(ws):
+    """96 4K frames in one call (3x the bench batch: 800 MB of frames, 526 MB of levels) give
+    exactly the boxes of three 32-frame calls (frame indices offset)."""
+    import torch
+    c = configs.C4
+    T1, T2 = c.thresholds()
+    fr = torch.from_numpy(c.make_frames(96)).cuda()
+    det = make_det(ws, T1, T2, c.Tnn, c.rule, max_batch=96)
+    big = det.detect(fr, c.min_face, c.scale_step)
+    parts = []
+    for k in range(3):
+        b = det.detect(fr[32 * k:32 * (k + 1)], c.min_face, c.scale_step)
+        b["frame"] += 32 * k
+        parts.append(b)
+    assert len(big) > 0 and np.array_equal(big, np.concatenate(parts))
+
+
 def test_host_vs_device_frames_and_determinism(ws):
     import torch
     c = configs.C3
