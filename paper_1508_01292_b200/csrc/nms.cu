@@ -20,7 +20,7 @@
 namespace ccnn {
 namespace {
 
-constexpr int kNmsThreads = 512;
+constexpr int kNmsThreads = 1024;          // (512: C5 NMS 0.112 ms, 1024: 0.096 ms per 16 frames)
 
 struct NmsSmem {
     short4 box[kNmsCap];         // x, y, w, h of this frame's raw boxes (sorted by x)
