@@ -263,7 +263,10 @@ __device__ __forceinline__ void prep_sample(int nc, uint8_t* ebuf, Prep* P)
     psync();
 }
 
-__global__ void __launch_bounds__(NT, 1) selective_cnn2_tc_kernel(
+// 72 registers (4 B of spill): 544 x 72 = 39k of the SM's 64k registers, so 5 CTAs of the next
+// batch's pyramid keep running beside a CNN2 CTA (at the default 96, 2): the pyramid no longer
+// stalls while the batch's tail holds the SMs -- C4 step 0.616 -> 0.601 ms (K3)
+__global__ void __maxnreg__(72) selective_cnn2_tc_kernel(
     const __grid_constant__ Cnn2Tc K, const SelParams sp, const uint16_t* __restrict__ bmats,
     const FrameInfo* __restrict__ frames, const LevelInfo* __restrict__ lvinfo,
     const S1Cand* __restrict__ cands, const uint32_t cand_cap, float* __restrict__ resp2,
