@@ -238,11 +238,13 @@ __device__ __forceinline__ void load_cols(const uint32_t* __restrict__ xt, int t
 }
 
 // GATHER class, SAFE tables (W, H >= 2: x0 + 1, y0 + 1 always inside): 4 byte gathers per
-// pixel from the frame through L1.  Register cap 40 (12 CTAs of 128 threads per SM): beside the
-// resident stage-1 CTA (320 threads x 120 registers) the register file then holds 6 pyramid CTAs
-// instead of 3 (56 registers uncapped); no spills.  Pipelined C4 step 0.65 -> 0.62 ms (K1)
+// pixel from the frame through L1.  Register cap 48 (10 CTAs of 128 threads per SM; 56 uncapped),
+// no spills: beside the resident stage-1 CTA (320 threads x 120 registers) or a CNN2 CTA (544 x
+// 72) the register file holds 4 pyramid CTAs instead of 3 (56) -- and each keeps more loads in
+// flight than at 40 registers (5 CTAs), which measured best: pipelined C4 step 0.650 (56) ->
+// 0.616 (40) -> 0.605 ms (48) (K1)
 #ifndef PYR_MINB
-#define PYR_MINB 12
+#define PYR_MINB 10
 #endif
 __global__ void __launch_bounds__(kPyrCols, PYR_MINB) pyramid_gather4_kernel(
     const FrameInfo* __restrict__ frames, uint8_t* __restrict__ levels,
